@@ -1,0 +1,232 @@
+/*
+ * include/rpq.h -- C-ABI of the B200-native RPQ / CRPQ hot path.
+ *
+ * Citations: PAPER.md = /root/reference/PAPER.md (cuRPQ, arXiv 2602.20748),
+ * "P:n" = line n.  SURVEY.md §8(b) lists these calls; DESIGN.md gives the
+ * readings (R1..R19) referred to below.
+ *
+ * Conventions (all functions):
+ *   - Return rpq_status (0 = OK, < 0 = error); nothing throws across the ABI.
+ *     On error every output handle is set to NULL and rpq_last_error() holds a
+ *     thread-local message.
+ *   - Inputs are caller-owned and copied (host arrays) or only read during
+ *     the call (device arrays).  Handles are library-owned and released by the
+ *     matching *_free.
+ *   - There is no CPU fallback: a call that needs the GPU returns RPQ_ECUDA
+ *     when no CUDA device is usable.  Only rpq_compile_labels, the rpq_nfa_*
+ *     queries and rpq_last_error run without a GPU.
+ *   - Vertex ids are u32 in [0, num_vertices) (vertex v_i has id i).
+ *   - Graphs and automata are immutable after creation; concurrent
+ *     evaluations on different streams may share them.
+ */
+#ifndef RPQ_H
+#define RPQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RPQ_OK = 0,
+    RPQ_EINVAL = -1,        /* bad argument / data (vertex id >= |V|, duplicate source, NULL) */
+    RPQ_ESYNTAX = -2,       /* regex syntax error (err_offset = byte offset) */
+    RPQ_ELABEL = -3,        /* regex names a label not in the vocabulary */
+    RPQ_ENOMEM = -4,        /* device or host allocation failed / budget too small */
+    RPQ_ECUDA = -5,         /* CUDA error or no usable device */
+    RPQ_ECAPACITY = -6,     /* caller buffer too small (required size returned) */
+    RPQ_EUNSUPPORTED = -7   /* automaton too large, disconnected CRPQ, ... */
+} rpq_status;
+
+typedef struct rpq_graph rpq_graph;
+typedef struct rpq_nfa rpq_nfa;
+typedef struct rpq_result rpq_result;
+
+/* ------------------------------------------------------------------------
+ * Graph: G = (V, E, L) with labelled vertices and edges.
+ * E is a SET of (u, label, w) triples (reading R4): duplicates collapse at
+ * load; self-loops are 1-hop paths (R5).  The device layout is one CSR per
+ * edge label ("a separate grid is maintained for each edge label"):
+ * off_l[|V|+1] (u32) and nbr_l[] (u32, ascending per row, 256-byte aligned
+ * base so rows can be read with 128-bit loads), plus the per-label
+ * [min, max] of source and destination ids.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    uint32_t num_vertices;
+    uint64_t num_edges;
+    const uint32_t *src;                    /* host [num_edges] */
+    const uint32_t *dst;                    /* host [num_edges] */
+    const uint16_t *label;                  /* host [num_edges], < num_labels */
+    uint32_t num_labels;
+    const char *const *label_names;         /* [num_labels] vocabulary for rpq_compile */
+    const uint16_t *vertex_label;           /* host [num_vertices] or NULL (CRPQ condition (1)) */
+    uint32_t num_vertex_labels;
+    const char *const *vertex_label_names;  /* [num_vertex_labels] or NULL */
+    int device;                             /* CUDA device ordinal */
+    uint32_t flags;                         /* reserved, 0 */
+    void *cuda_stream;                      /* cudaStream_t used for the build, NULL = default */
+} rpq_graph_desc;
+
+/* Copies the host arrays to the device and builds the per-label CSR.
+ * Errors: EINVAL (id >= num_vertices, label >= num_labels, NULL arrays with
+ * num_edges > 0), ENOMEM, ECUDA (no device).  One-time; not part of query
+ * time (the paper excludes loading). */
+rpq_status rpq_graph_load(const rpq_graph_desc *desc, rpq_graph **out);
+void rpq_graph_free(rpq_graph *g);
+/* |V|, number of DISTINCT (u,l,w) triples, number of labels */
+rpq_status rpq_graph_info(const rpq_graph *g, uint32_t *num_vertices, uint64_t *num_edges,
+                          uint32_t *num_labels);
+/* Device views (valid until rpq_graph_free) of label l's CSR. */
+rpq_status rpq_graph_label_csr(const rpq_graph *g, uint32_t label, const uint32_t **off,
+                               const uint32_t **nbr, uint64_t *num_edges);
+
+/* ------------------------------------------------------------------------
+ * rpq_compile: regex over edge labels -> automaton (the "automata plan" of
+ * P:253-259; Fig. 2(a) gives abc* as q0 -a-> q1 -b-> q2 with a c-loop).
+ * Host-side.  Route: tokenise (longest match against the vocabulary, R3) ->
+ * parse ('|' alternation, postfix * + ?, R2) -> Glushkov position NFA ->
+ * subset construction -> Hopcroft minimisation -> trim (dead and unreachable
+ * states removed) -> canonical numbering (BFS from the initial state 0).
+ * If the minimal DFA has more than RPQ_MAX_STATES states the trimmed
+ * Glushkov NFA is used instead (same result set, different PE).
+ * flags: RPQ_SYNTAX_PAPER -> infix '+' is alternation (tab:queries,
+ * P:1042-1043); RPQ_NO_MINIMIZE -> keep the Glushkov NFA (tests).
+ * Errors: ESYNTAX (*err_offset = byte offset), ELABEL (*err_offset = offset
+ * of the unknown name), EUNSUPPORTED (> RPQ_MAX_STATES states). */
+#define RPQ_SYNTAX_PAPER 1u
+#define RPQ_NO_MINIMIZE 2u
+#define RPQ_MAX_STATES 64
+#define RPQ_MAX_TRANSITIONS 256
+#define RPQ_MAX_QUERY_LABELS 32
+rpq_status rpq_compile(const rpq_graph *vocab, const char *regex, uint32_t flags,
+                       rpq_nfa **out, size_t *err_offset);
+/* Same, with an explicit vocabulary (no graph, no GPU needed). */
+rpq_status rpq_compile_labels(const char *const *label_names, uint32_t num_labels,
+                              const char *regex, uint32_t flags, rpq_nfa **out,
+                              size_t *err_offset);
+void rpq_nfa_free(rpq_nfa *a);
+rpq_status rpq_nfa_info(const rpq_nfa *a, uint32_t *num_states, uint32_t *num_transitions,
+                        uint32_t *num_final, int *accepts_empty, int *is_dfa);
+/* transitions (from, label, to) sorted by (from, label, to); *n = count
+ * (ECAPACITY if cap < count); final states as a bit mask */
+rpq_status rpq_nfa_transitions(const rpq_nfa *a, uint32_t *from, uint32_t *label, uint32_t *to,
+                               uint32_t cap, uint32_t *n, uint64_t *final_mask);
+/* word membership (host simulation; used to pin the compiler) */
+rpq_status rpq_nfa_accepts(const rpq_nfa *a, const uint32_t *word, uint32_t len, int *accepted);
+
+/* ------------------------------------------------------------------------
+ * Evaluation (Definition 1): R(rho) = distinct (x, y) such that a
+ * path x -> ... -> y has a label word in L(rho).  epsilon in L(rho) => (v, v)
+ * for every source v (reading R1).  Method: level-synchronous multi-source
+ * BFS over the product graph G x A(rho) with a per-source
+ * visited set over (vertex, state) kept as bit-parallel words: source batches
+ * of B sources, one bit per source, B sized against the HBM budget
+ * (Challenge 2).
+ * ------------------------------------------------------------------------ */
+#define RPQ_COUNT 1u          /* total number of result pairs (the paper's output) */
+#define RPQ_PAIRS 2u          /* materialise sorted distinct (src, dst) pairs */
+#define RPQ_PER_SOURCE 4u     /* per-source result counts */
+#define RPQ_STATS 8u          /* count PE / word ops / items (small overhead) */
+#define RPQ_TIME_KERNELS 16u  /* CUDA-event time of every expand launch */
+
+typedef struct {
+    uint32_t mode;              /* OR of the RPQ_* mode bits above; 0 = RPQ_COUNT */
+    uint32_t batch_sources;     /* B; 0 = auto (HBM budget), rounded up to 64 */
+    uint64_t hbm_budget_bytes;  /* 0 = 90% of free device memory */
+    uint32_t shard_index;       /* evaluate batches b with b % shard_count == shard_index */
+    uint32_t shard_count;       /* 0 or 1 = unsharded */
+    void *cuda_stream;          /* cudaStream_t; NULL = default stream */
+    uint32_t chunk_words;       /* 0 = auto; else words per work item (1,2,4,8,16,32) */
+    uint32_t reserved;
+} rpq_eval_opts;
+
+/* All-pairs: x ranges over all of V (R11).  With shard_count > 1 the result
+ * holds only this shard's batches (sources are cut into batches of B
+ * consecutive productive sources; batch b belongs to shard b % count). */
+rpq_status rpq_eval_allpairs(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
+                             rpq_result **out);
+/* Single source x = src.  src >= |V| -> EINVAL. */
+rpq_status rpq_eval_single_source(const rpq_graph *g, const rpq_nfa *a, uint32_t src,
+                                  const rpq_eval_opts *opts, rpq_result **out);
+/* A set of sources (host array, any order, no duplicates -> else EINVAL).
+ * Pairs are sorted by (src, dst) regardless of input order. */
+rpq_status rpq_eval_sources(const rpq_graph *g, const rpq_nfa *a, const uint32_t *srcs,
+                            uint64_t n, const rpq_eval_opts *opts, rpq_result **out);
+
+/* ------------------------------------------------------------------------
+ * CRPQ (Definition 2): all homomorphisms f: V_q -> V with
+ * (1) L(f(u)) = L_q(u) where a label is given, (2) (f(x), f(y)) in R(rho) for
+ * every atom x -rho-> y; plus optional distinct-vertex filters (CQ4/CQ5,
+ * P:1085).  Atoms are evaluated with the RPQ kernels (sources restricted to
+ * candidates), then joined on the device.  Tuples are distinct and sorted
+ * lexicographically in variable order.  A variable in no atom or a
+ * disconnected pattern -> EUNSUPPORTED (reading R18).
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    uint32_t num_vars;
+    const int32_t *var_label;        /* [num_vars] vertex-label id or -1 (any) */
+    const int64_t *var_const;        /* [num_vars] vertex id or -1 (free) */
+    uint32_t num_atoms;
+    const uint32_t *atom_x;          /* [num_atoms] variable ids */
+    const uint32_t *atom_y;
+    const rpq_nfa *const *atom_nfa;  /* [num_atoms] */
+    uint32_t num_distinct;
+    const uint32_t *distinct_pairs;  /* [2*num_distinct] variable ids */
+} crpq_query;
+rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts,
+                     rpq_result **out);
+
+/* ------------------------------------------------------------------------
+ * Results.  Pair results have 2 columns (src, dst); CRPQ results one column
+ * per variable.  Rows are distinct and sorted.  Device views stay valid
+ * until rpq_result_free.
+ * ------------------------------------------------------------------------ */
+#define RPQ_MAX_COLS 16
+typedef struct {
+    uint64_t count;             /* result pairs / tuples */
+    uint64_t product_edges;     /* PE: sum over reached (v,q) of product out-degree (RPQ_STATS) */
+    uint64_t word_items;        /* non-zero 64-bit frontier words expanded */
+    uint64_t word_edge_ops;     /* (non-zero frontier word) x (edge) operations */
+    uint64_t items;             /* work items (chunk of words, state, vertex) expanded */
+    uint64_t item_edges;        /* (item) x (edge) pairs = neighbour ids read */
+    uint64_t item_transitions;  /* (item) x (automaton transition) pairs = offset pairs read */
+    uint64_t activations;       /* red.or on the activity bitmap (row, chunk) */
+    uint64_t next_reds;         /* red.or on the next-frontier words */
+    uint32_t levels;            /* BFS levels summed over batches */
+    uint32_t batches;           /* batches evaluated by this shard */
+    uint32_t batch_sources;     /* B */
+    uint32_t chunk_words;       /* words per work item */
+    uint64_t productive_sources;/* |P| over the whole query (all shards) */
+    uint64_t state_words;       /* 64-bit words per state array */
+    uint64_t expand_launches;   /* expand-kernel launches (main + hub) */
+    uint64_t kernel_launches;   /* all kernels this library launched for the call */
+    double expand_ms;           /* RPQ_TIME_KERNELS: summed CUDA-event time of expand launches */
+    double total_ms;            /* CUDA-event time from entry to result ready */
+} rpq_stats;
+
+uint64_t rpq_result_count(const rpq_result *r);
+rpq_status rpq_result_device_view(const rpq_result *r, const uint32_t **cols, uint32_t *ncols,
+                                  uint64_t *n);
+/* copies rows to host column buffers cols[0..ncols-1] of capacity cap rows;
+ * ECAPACITY (and *n = required) if cap < rows */
+rpq_status rpq_result_copy_host(const rpq_result *r, uint32_t *const *cols, uint64_t cap,
+                                uint64_t *n);
+/* RPQ_PER_SOURCE: (source, count) for every source of this shard with a
+ * non-zero count, ascending source; host buffers, ECAPACITY as above */
+rpq_status rpq_result_source_counts(const rpq_result *r, uint32_t *srcs, uint64_t *counts,
+                                    uint64_t cap, uint64_t *n);
+rpq_status rpq_result_stats(const rpq_result *r, rpq_stats *s);
+void rpq_result_free(rpq_result *r);
+
+const char *rpq_last_error(void);
+/* number of usable CUDA devices (0 on a machine without a GPU) */
+rpq_status rpq_device_count(int *n);
+/* library build string (arch, version) */
+const char *rpq_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RPQ_H */

@@ -1,0 +1,185 @@
+// C-ABI plumbing: errors, automaton queries, result accessors, allocator.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+
+static thread_local std::string g_last_error;
+
+rpq_status rpq_fail(rpq_status st, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return st;
+}
+
+void rpq_clear_error() { g_last_error.clear(); }
+
+extern "C" const char *rpq_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char *rpq_version(void) {
+    return "rpq-b200 0.1 (sm_100a; per-label CSR; bit-parallel multi-source product BFS)";
+}
+
+extern "C" rpq_status rpq_device_count(int *n) {
+    if (!n) return rpq_fail(RPQ_EINVAL, "NULL");
+    *n = 0;
+    cudaError_t e = cudaGetDeviceCount(n);
+    if (e != cudaSuccess) { *n = 0; cudaGetLastError(); }
+    return RPQ_OK;
+}
+
+// ---- stream-ordered device allocation -----------------------------------
+// cudaMallocAsync from the device's default pool with an unbounded release
+// threshold: freed blocks stay reserved, so the per-query state arrays are
+// recycled without cudaMalloc/cudaFree page-mapping costs.
+static std::once_flag g_pool_once[64];
+
+void *dev_alloc(size_t bytes, void *stream) {
+    if (bytes == 0) bytes = 16;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::call_once(g_pool_once[dev & 63], [dev]() {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, bytes, (cudaStream_t)stream) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void dev_free(void *p, void *stream) {
+    if (p) cudaFreeAsync(p, (cudaStream_t)stream);
+}
+
+// ---- automaton -----------------------------------------------------------
+extern "C" rpq_status rpq_compile(const rpq_graph *vocab, const char *regex, uint32_t flags,
+                                  rpq_nfa **out, size_t *err_offset) {
+    if (out) *out = nullptr;
+    if (!vocab) return rpq_fail(RPQ_EINVAL, "rpq_compile: NULL graph");
+    return compile_regex(vocab->label_names, regex, flags, out, err_offset);
+}
+
+extern "C" rpq_status rpq_compile_labels(const char *const *names, uint32_t n, const char *regex,
+                                         uint32_t flags, rpq_nfa **out, size_t *err_offset) {
+    if (out) *out = nullptr;
+    if (n && !names) return rpq_fail(RPQ_EINVAL, "rpq_compile_labels: NULL names");
+    std::vector<std::string> v;
+    for (uint32_t i = 0; i < n; ++i) v.emplace_back(names[i] ? names[i] : "");
+    return compile_regex(v, regex, flags, out, err_offset);
+}
+
+extern "C" void rpq_nfa_free(rpq_nfa *a) { delete a; }
+
+extern "C" rpq_status rpq_nfa_info(const rpq_nfa *a, uint32_t *nq, uint32_t *nt, uint32_t *nf,
+                                   int *acc_empty, int *is_dfa) {
+    if (!a) return rpq_fail(RPQ_EINVAL, "NULL automaton");
+    if (nq) *nq = a->nq;
+    if (nt) *nt = (uint32_t)a->from.size();
+    if (nf) *nf = (uint32_t)__builtin_popcountll(a->final_mask);
+    if (acc_empty) *acc_empty = a->accepts_empty;
+    if (is_dfa) *is_dfa = a->is_dfa;
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_nfa_transitions(const rpq_nfa *a, uint32_t *from, uint32_t *label,
+                                          uint32_t *to, uint32_t cap, uint32_t *n,
+                                          uint64_t *final_mask) {
+    if (!a) return rpq_fail(RPQ_EINVAL, "NULL automaton");
+    uint32_t cnt = (uint32_t)a->from.size();
+    if (n) *n = cnt;
+    if (final_mask) *final_mask = a->final_mask;
+    if (cap < cnt) return cap == 0 && !from ? RPQ_OK : rpq_fail(RPQ_ECAPACITY, "need %u", cnt);
+    for (uint32_t i = 0; i < cnt; ++i) {
+        if (from) from[i] = a->from[i];
+        if (label) label[i] = a->label[i];
+        if (to) to[i] = a->to[i];
+    }
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_nfa_accepts(const rpq_nfa *a, const uint32_t *word, uint32_t len,
+                                      int *accepted) {
+    if (!a || !accepted || (len && !word)) return rpq_fail(RPQ_EINVAL, "NULL argument");
+    uint64_t cur = a->nq ? 1ull : 0ull;
+    for (uint32_t i = 0; i < len && cur; ++i) {
+        uint64_t nxt = 0;
+        for (uint32_t q = 0; q < a->nq; ++q) if ((cur >> q) & 1)
+            for (uint32_t t = a->off[q]; t < a->off[q + 1]; ++t)
+                if (a->label[t] == word[i]) nxt |= 1ull << a->to[t];
+        cur = nxt;
+    }
+    *accepted = (cur & a->final_mask) != 0;
+    return RPQ_OK;
+}
+
+// ---- results -------------------------------------------------------------
+void rpq_result_release(rpq_result *r) {
+    if (!r) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(r->device);
+    for (uint32_t c = 0; c < RPQ_MAX_COLS; ++c) if (r->cols[c]) cudaFree(r->cols[c]);
+    if (r->ps_src) cudaFree(r->ps_src);
+    if (r->ps_cnt) cudaFree(r->ps_cnt);
+    cudaSetDevice(prev);
+    delete r;
+}
+
+extern "C" void rpq_result_free(rpq_result *r) { rpq_result_release(r); }
+
+extern "C" uint64_t rpq_result_count(const rpq_result *r) { return r ? r->count : 0; }
+
+extern "C" rpq_status rpq_result_device_view(const rpq_result *r, const uint32_t **cols,
+                                             uint32_t *ncols, uint64_t *n) {
+    if (!r) return rpq_fail(RPQ_EINVAL, "NULL result");
+    if (ncols) *ncols = r->ncols;
+    if (n) *n = r->nrows;
+    if (cols) for (uint32_t c = 0; c < r->ncols; ++c) cols[c] = r->cols[c];
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_result_copy_host(const rpq_result *r, uint32_t *const *cols, uint64_t cap,
+                                           uint64_t *n) {
+    if (!r) return rpq_fail(RPQ_EINVAL, "NULL result");
+    if (n) *n = r->nrows;
+    if (cap < r->nrows) return rpq_fail(RPQ_ECAPACITY, "need %llu rows", (unsigned long long)r->nrows);
+    if (!cols && r->nrows) return rpq_fail(RPQ_EINVAL, "NULL columns");
+    cudaSetDevice(r->device);
+    for (uint32_t c = 0; c < r->ncols; ++c)
+        if (r->nrows) RPQ_CUDA_TRY(cudaMemcpy(cols[c], r->cols[c], r->nrows * 4, cudaMemcpyDeviceToHost));
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_result_source_counts(const rpq_result *r, uint32_t *srcs, uint64_t *counts,
+                                               uint64_t cap, uint64_t *n) {
+    if (!r) return rpq_fail(RPQ_EINVAL, "NULL result");
+    if (n) *n = r->n_ps;
+    if (cap < r->n_ps) return rpq_fail(RPQ_ECAPACITY, "need %llu", (unsigned long long)r->n_ps);
+    cudaSetDevice(r->device);
+    if (r->n_ps) {
+        if (srcs) RPQ_CUDA_TRY(cudaMemcpy(srcs, r->ps_src, r->n_ps * 4, cudaMemcpyDeviceToHost));
+        if (counts) RPQ_CUDA_TRY(cudaMemcpy(counts, r->ps_cnt, r->n_ps * 8, cudaMemcpyDeviceToHost));
+    }
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_result_stats(const rpq_result *r, rpq_stats *s) {
+    if (!r || !s) return rpq_fail(RPQ_EINVAL, "NULL argument");
+    *s = r->stats;
+    s->count = r->count;
+    return RPQ_OK;
+}

@@ -1,0 +1,1055 @@
+// RPQ evaluation on sm_100a: level-synchronous, bit-parallel multi-source
+// BFS over the product graph G x A(rho).
+//
+// PAPER.md (P:n = line n of /root/reference/PAPER.md):
+//   Definition 1: the result is the set of DISTINCT (x, y) such
+//     that a path x -> ... -> y has a label word in L(rho).
+//   Automata-based approach: traverse (vertex, state) pairs from
+//     (x, q_init); a per-source visited set over (vertex, state) keeps the
+//     output distinct and the traversal finite; a pair is emitted when a
+//     final state is reached.
+//   Challenge 2: the visited set costs |V||Q|/8 bytes per source;
+//     the number of concurrent sources is bounded by memory.
+//
+// B200 design (DESIGN.md has the full rationale and the roofline):
+//   * One bit per source.  A batch of B sources is a column block of
+//     nw = ceil(B/64) 64-bit words.  Three state arrays Vis, F (frontier),
+//     N (next frontier), row-major: word[row * nw + w], one row per
+//     (state q, vertex v in range_q); range_q is the hull of the destination
+//     ranges of the labels entering q (plus the batch's sources for q0), so
+//     states that only live on a label-contiguous vertex block only pay for it.
+//   * A work item is (q, v, chunk) where a chunk is CW consecutive words of
+//     the row; a group of CW lanes expands it: every lane owns one word, the
+//     group walks the per-label CSR rows of v once and each lane updates its
+//     word of the target row (coalesced CW*8-byte segments).
+//   * Discovery is fused: old = atomicOr(Vis[t], f & ~Vis[t]); the truly new
+//     bits go to N[t] with a second atomicOr.  Vis is therefore exact at the
+//     end of every level and no separate "advance" pass exists.  A (row,
+//     chunk) item whose N chunk becomes non-zero is appended once to the next
+//     worklist (activity bitmap, test-before-atomic, warp-aggregated append).
+//   * F words are cleared as they are read, so F and N swap roles each level.
+//   * Rows with more than HUB_EDGES neighbours for a transition are split
+//     into HUB_EDGES segments processed by a second kernel (degree skew).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <vector>
+
+#include "internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace {
+
+constexpr int MAXQ = RPQ_MAX_STATES;
+constexpr int MAXT = RPQ_MAX_TRANSITIONS;
+constexpr int MAXL = RPQ_MAX_QUERY_LABELS;
+constexpr uint32_t HUB_EDGES = 512;      // edges per hub segment
+constexpr int TILE_V = 1024;             // vertices per extraction tile
+constexpr int NSTAT = 8;
+
+struct DevAuto {
+    uint32_t nq;
+    uint64_t final_mask;
+    uint16_t toff[MAXQ + 1];
+    uint8_t tslot[MAXT];
+    uint8_t tto[MAXT];
+    const uint32_t *off[MAXL];
+    const uint32_t *nbr[MAXL];
+};
+
+struct Layout {
+    uint64_t row_base[MAXQ];   // first row of state q
+    uint32_t lo[MAXQ];         // range_q = [lo, lo + len)
+    uint32_t len[MAXQ];
+};
+
+struct Item {
+    uint32_t v;
+    uint32_t qc;               // q << 24 | chunk
+};
+
+struct HubRec {                // one HUB_EDGES-edge segment of a long CSR row
+    uint32_t v, qc;            // item
+    uint32_t t;                // automaton transition
+    uint32_t beg, end;         // CSR edge range
+};
+
+struct Ctrl {                  // per-level counters (device)
+    uint32_t cnt[2];           // worklist sizes (ping-pong)
+    uint32_t nhub_recs;
+    uint32_t pad;
+};
+
+struct ExpandArgs {
+    const uint64_t *F;         // frontier words (read-only during expand)
+    uint64_t *N;               // next-frontier accumulator (red.or targets)
+    const uint64_t *Vis;       // visited words (read-only during expand)
+    uint32_t *X;               // activity bitmap over (row, chunk)
+    const Item *cur;
+    Ctrl *ctrl;
+    int cur_idx;               // ctrl->cnt[cur_idx] = items in cur
+    HubRec *hrecs;
+    uint32_t hrec_cap;
+    uint32_t nw, nchunk;
+    unsigned long long *stats;
+};
+
+// stats slots
+enum { S_PE = 0, S_WORD_ITEMS, S_WORD_EDGE, S_ITEMS, S_ITEM_EDGES, S_ITEM_TRANS, S_X_RED, S_N_RED };
+
+__device__ __forceinline__ uint64_t ld_cg(const uint64_t *p) { return __ldcg((const unsigned long long *)p); }
+
+// fire-and-forget OR into global memory (RED.E.OR.64: no return value, so
+// the issuing warp never waits for the L2 round trip)
+__device__ __forceinline__ void red_or64(uint64_t *p, uint64_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_or32(uint32_t *p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Expand one (item, transition) over CSR edges [beg, end) for a group of CW
+// lanes; f is this lane's frontier word.  Per target row: m = f & ~Vis;
+// N |= m (red.or); mark (row, chunk) active in X (test, then red.or).
+template <int CW, bool STATS>
+__device__ __forceinline__ void expand_edges(const ExpandArgs &p, const DevAuto &A, const Layout &S, int t,
+                                             uint32_t beg, uint32_t end, uint64_t f, uint32_t c,
+                                             unsigned gmask, int gl, unsigned long long *st) {
+    const int slot = A.tslot[t];
+    const uint32_t q2 = A.tto[t];
+    const uint32_t *__restrict__ nbr = A.nbr[slot];
+    const uint64_t tbase = S.row_base[q2] - S.lo[q2];
+    const uint64_t col = (uint64_t)c * CW + gl;
+    const int fpop = __popcll(f);
+    constexpr int R = CW >= 8 ? 1 : 8 / CW;   // neighbour ids held per lane
+    constexpr int EPI = CW * R;               // edges per iteration (multiple of 8)
+    for (uint32_t j = beg; j < end; j += EPI) {
+        uint32_t mine[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            uint32_t idx = j + r * CW + gl;
+            mine[r] = idx < end ? __ldg(nbr + idx) : 0u;
+        }
+        const int cnt = (int)((end - j) < (uint32_t)EPI ? (end - j) : (uint32_t)EPI);
+        for (int k0 = 0; k0 < cnt; k0 += 8) {
+            uint64_t trow[8], vis[8];
+            uint32_t xw[8];
+            // issue all loads of the 8 targets before any dependent work
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int k = k0 + u;
+                uint32_t w;
+                if constexpr (CW >= 8) w = __shfl_sync(gmask, mine[0], k & (CW - 1), CW);
+                else w = __shfl_sync(gmask, mine[(u / CW) % R], u % CW, CW);
+                trow[u] = tbase + w;
+                vis[u] = (f && k < cnt) ? __ldg((const unsigned long long *)(p.Vis + trow[u] * p.nw + col)) : ~0ull;
+                const uint64_t bi = trow[u] * p.nchunk + c;
+                xw[u] = (gl == 0 && k < cnt) ? __ldcg(p.X + (bi >> 5)) : ~0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t m = f & ~vis[u];
+                if (m) red_or64(p.N + trow[u] * p.nw + col, m);
+                const unsigned am = __ballot_sync(gmask, m != 0) & gmask;
+                if (am && gl == 0) {
+                    const uint64_t bi = trow[u] * p.nchunk + c;
+                    const uint32_t bit = 1u << (bi & 31);
+                    if (!(xw[u] & bit)) {
+                        red_or32(p.X + (bi >> 5), bit);
+                        if (STATS) st[S_X_RED]++;
+                    }
+                }
+                if (STATS && m) st[S_N_RED]++;
+            }
+        }
+        if (STATS && f) {
+            st[S_WORD_EDGE] += cnt;
+            st[S_PE] += (unsigned long long)fpop * cnt;
+        }
+        if (STATS && gl == 0) st[S_ITEM_EDGES] += cnt;
+    }
+}
+
+template <bool STATS>
+__device__ __forceinline__ void flush_stats(unsigned long long *st, unsigned long long *out) {
+    if constexpr (!STATS) return;
+    else {
+#pragma unroll
+    for (int i = 0; i < NSTAT; ++i) {
+        unsigned long long x = st[i];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, x);
+    }
+    }
+}
+
+template <int CW, bool STATS>
+__global__ void __launch_bounds__(256) k_expand(const DevAuto A, const Layout S, const ExpandArgs p) {
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (CW - 1);
+    const unsigned gmask = CW == 32 ? 0xffffffffu : (((1u << CW) - 1u) << (lane & ~(CW - 1)));
+    const uint64_t ngroups = (uint64_t)gridDim.x * blockDim.x / CW;
+    const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / CW;
+    const uint32_t n = p.ctrl->cnt[p.cur_idx];
+    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // all lanes of a warp run the same number of outer iterations so that the
+    // final stats reduction is warp-uniform; groups past n idle.
+    const uint64_t wfirst = gid - (uint64_t)(lane / CW);
+    for (uint64_t base = wfirst; base < n; base += ngroups) {
+        const uint64_t it = base + (uint64_t)(lane / CW);
+        if (it >= n) continue;   // whole group skips together
+        const Item item = p.cur[it];
+        const uint32_t v = item.v, q = item.qc >> 24, c = item.qc & 0xffffffu;
+        const uint64_t row = S.row_base[q] + (v - S.lo[q]);
+        const uint64_t f = p.F[row * p.nw + (uint64_t)c * CW + gl];
+        if (STATS && gl == 0) st[S_ITEMS]++;
+        if (STATS && f) st[S_WORD_ITEMS]++;
+        for (int t = A.toff[q]; t < A.toff[q + 1]; ++t) {
+            const uint32_t *off = A.off[A.tslot[t]];
+            const uint32_t beg = __ldg(off + v), end = __ldg(off + v + 1);
+            if (STATS && gl == 0) st[S_ITEM_TRANS]++;
+            if (end == beg) continue;
+            if (end - beg > HUB_EDGES) {
+                // long row: one record per HUB_EDGES-edge segment, expanded by
+                // k_expand_hub (F is read-only during the level, so the hub
+                // kernel reads the frontier words itself)
+                const uint32_t nseg = (end - beg + HUB_EDGES - 1) / HUB_EDGES;
+                uint32_t r = 0;
+                if (gl == 0) r = atomicAdd(&p.ctrl->nhub_recs, nseg);
+                r = __shfl_sync(gmask, r, 0, CW);
+                if (r + nseg <= p.hrec_cap) {
+                    for (uint32_t s = gl; s < nseg; s += CW) {
+                        const uint32_t b = beg + s * HUB_EDGES;
+                        p.hrecs[r + s] = HubRec{v, item.qc, (uint32_t)t, b, min(end, b + HUB_EDGES)};
+                    }
+                    continue;
+                }
+                // overflow: neutralise the reserved records, expand inline
+                for (uint32_t s = gl; r + s < p.hrec_cap && s < nseg; s += CW)
+                    p.hrecs[r + s] = HubRec{0u, 0u, 0u, 0u, 0u};
+            }
+            expand_edges<CW, STATS>(p, A, S, t, beg, end, f, c, gmask, gl, st);
+        }
+    }
+    flush_stats<STATS>(st, p.stats);
+}
+
+template <int CW, bool STATS>
+__global__ void __launch_bounds__(256) k_expand_hub(const DevAuto A, const Layout S, const ExpandArgs p) {
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (CW - 1);
+    const unsigned gmask = CW == 32 ? 0xffffffffu : (((1u << CW) - 1u) << (lane & ~(CW - 1)));
+    const uint64_t ngroups = (uint64_t)gridDim.x * blockDim.x / CW;
+    const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / CW;
+    const uint32_t n = min(p.ctrl->nhub_recs, p.hrec_cap);
+    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint64_t wfirst = gid - (uint64_t)(lane / CW);
+    for (uint64_t base = wfirst; base < n; base += ngroups) {
+        const uint64_t it = base + (uint64_t)(lane / CW);
+        if (it >= n) continue;
+        const HubRec r = p.hrecs[it];
+        if (r.end == r.beg) continue;
+        const uint32_t q = r.qc >> 24, c = r.qc & 0xffffffu;
+        const uint64_t row = S.row_base[q] + (r.v - S.lo[q]);
+        const uint64_t f = p.F[row * p.nw + (uint64_t)c * CW + gl];
+        expand_edges<CW, STATS>(p, A, S, (int)r.t, r.beg, r.end, f, c, gmask, gl, st);
+    }
+    flush_stats<STATS>(st, p.stats);
+}
+
+// Advance (end of a level): for every active (row, chunk) of X:
+//   n = N & ~Vis; F = n; Vis |= n; N = 0; X bit cleared;
+// and append the item to the next worklist if n != 0.  A warp takes one X
+// word (32 items); its CW-lane groups take the set bits.
+template <int CW>
+__global__ void __launch_bounds__(256) k_advance(const DevAuto A, const Layout S, uint64_t *F, uint64_t *N,
+                                                 uint64_t *Vis, uint32_t *X, uint64_t xwords, uint32_t nw,
+                                                 uint32_t nchunk, uint32_t nq, Item *next, uint32_t *next_cnt) {
+    constexpr int G = 32 / CW;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane & (CW - 1), grp = lane / CW;
+    const unsigned gmask = CW == 32 ? 0xffffffffu : (((1u << CW) - 1u) << (lane & ~(CW - 1)));
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    for (uint64_t xi = wid; xi < xwords; xi += nwarps) {
+        uint32_t x = __ldcg(X + xi);
+        if (!x) continue;
+        if (lane == 0) X[xi] = 0;
+        // the set bits are shared out G per round
+        while (x) {
+            // group grp takes the grp-th lowest set bit of x (if any)
+            uint32_t y = x;
+            for (int k = 0; k < grp && y; ++k) y &= y - 1;
+            const bool has = y != 0;
+            const int b = has ? __ffs(y) - 1 : 0;
+            for (int k = 0; k < G && x; ++k) x &= x - 1;   // drop the bits taken this round
+            if (!has) continue;
+            const uint64_t it = xi * 32 + b;
+            const uint64_t row = it / nchunk;
+            const uint32_t c = (uint32_t)(it % nchunk);
+            const uint64_t wi = row * nw + (uint64_t)c * CW + gl;
+            uint64_t n = N[wi];
+            uint64_t vis = Vis[wi];
+            n &= ~vis;
+            F[wi] = n;
+            if (n) Vis[wi] = vis | n;
+            N[wi] = 0;
+            const unsigned any = __ballot_sync(gmask, n != 0) & gmask;
+            if (any && gl == 0) {
+                int q = 0;
+                while (q + 1 < (int)nq && S.row_base[q + 1] <= row) ++q;
+                const uint32_t v = S.lo[q] + (uint32_t)(row - S.row_base[q]);
+                cg::coalesced_group g = cg::coalesced_threads();
+                uint32_t pos = 0;
+                if (g.thread_rank() == 0) pos = atomicAdd(next_cnt, (uint32_t)g.size());
+                pos = g.shfl(pos, 0) + g.thread_rank();
+                next[pos] = Item{v, ((uint32_t)q << 24) | c};
+            }
+        }
+    }
+}
+
+// Seed batch sources: source i of the batch gets bit i in F and Vis of row
+// (q0, s_i); one item per source (rows are distinct, so no atomics).  The
+// whole CW-word chunk of F is written (F is never bulk-cleared).
+template <int CW>
+__global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const uint32_t *__restrict__ pidx,
+                       uint64_t b0, uint32_t nb, uint64_t *F, uint64_t *Vis, Item *cur, Ctrl *ctrl, uint32_t nw) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+        const uint32_t s = cand[pidx[b0 + i]];
+        const uint64_t row = S.row_base[0] + (s - S.lo[0]);
+        const uint32_t w = i >> 6, c = w / CW;
+        const uint64_t bit = 1ull << (i & 63);
+#pragma unroll
+        for (int k = 0; k < CW; ++k) F[row * nw + (uint64_t)c * CW + k] = (c * CW + k == w) ? bit : 0ull;
+        Vis[row * nw + w] = bit;
+        cur[i] = Item{s, (0u << 24) | c};
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctrl->cnt[0] = nb;
+        ctrl->cnt[1] = 0;
+        ctrl->nhub_recs = 0;
+    }
+}
+
+// ---- productive sources: s with an out-edge under a label leaving q0 ------
+__global__ void k_productive(const DevAuto A, const uint32_t *__restrict__ cand, uint64_t n, uint8_t *flag) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t s = cand[j];
+        uint8_t f = 0;
+        for (int t = A.toff[0]; t < A.toff[1] && !f; ++t) {
+            const uint32_t *off = A.off[A.tslot[t]];
+            f = __ldg(off + s + 1) > __ldg(off + s);
+        }
+        flag[j] = f;
+    }
+}
+
+__global__ void k_iota(uint32_t *x, uint64_t n) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+        x[j] = (uint32_t)j;
+}
+
+// ---- extraction ------------------------------------------------------------
+// Ans(v, w) = OR over final states q with v in range_q of Vis[row(q,v), w]:
+// OR-ing the final states deduplicates targets reached in several final
+// states (distinct pairs).
+__device__ __forceinline__ uint64_t ans_word(const DevAuto &A, const Layout &S, const uint64_t *Vis,
+                                             uint32_t v, uint64_t w, uint32_t nw) {
+    uint64_t acc = 0;
+    uint64_t fm = A.final_mask;
+    while (fm) {
+        const int q = __ffsll((long long)fm) - 1;
+        fm &= fm - 1;
+        if (v - S.lo[q] < S.len[q]) acc |= ld_cg(Vis + (S.row_base[q] + (v - S.lo[q])) * nw + w);
+    }
+    return acc;
+}
+
+// COUNT: total popcount of Ans over the hull [vlo, vlo + vn) x [0, nw).
+__global__ void k_count_total(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
+                              uint32_t nw, unsigned long long *total) {
+    unsigned long long acc = 0;
+    const uint64_t n = vn * nw;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = vlo + (uint32_t)(i / nw);
+        acc += __popcll(ans_word(A, S, Vis, v, i % nw, nw));
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, acc);
+}
+
+// Per-(source, tile) counts by warp ballot transposes: a warp takes a tile of
+// TILE_V vertices and a group of 4 words (32 B = one sector per row); lane l
+// holds vertex v0 + l; ballot over bit b gives the tile's members of source
+// w*64+b.  cnt[(i) * nseg + seg] (u32), i = batch-local source index.
+__global__ void k_tile_counts(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
+                              uint32_t nw, uint32_t nb, uint32_t nseg, uint32_t *cnt) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwg = (nw + 3) / 4;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    for (uint64_t task = wid; task < (uint64_t)nseg * nwg; task += nwarps) {
+        const uint32_t seg = (uint32_t)(task / nwg);
+        const uint32_t w0 = (uint32_t)(task % nwg) * 4;
+        uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const uint64_t vbeg = (uint64_t)seg * TILE_V, vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
+        for (uint64_t v0 = vbeg; v0 < vend; v0 += 32) {
+            const uint64_t vv = v0 + lane;
+            uint64_t x[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                x[k] = (vv < vend && w0 + k < nw) ? ans_word(A, S, Vis, vlo + (uint32_t)vv, w0 + k, nw) : 0ull;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!__ballot_sync(0xffffffffu, x[k] != 0)) continue;
+                const uint32_t lo = (uint32_t)x[k], hi = (uint32_t)(x[k] >> 32);
+#pragma unroll 8
+                for (int b = 0; b < 32; ++b) {
+                    const unsigned m0 = __ballot_sync(0xffffffffu, (lo >> b) & 1u);
+                    const unsigned m1 = __ballot_sync(0xffffffffu, (hi >> b) & 1u);
+                    if (lane == b) { c[2 * k] += __popc(m0); c[2 * k + 1] += __popc(m1); }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i0 = (w0 + k) * 64 + lane, i1 = i0 + 32;
+            if (i0 < nb) cnt[(uint64_t)i0 * nseg + seg] = c[2 * k];
+            if (i1 < nb) cnt[(uint64_t)i1 * nseg + seg] = c[2 * k + 1];
+        }
+    }
+}
+
+// Row-wise exclusive scan of cnt[i][0..nseg) (in place) -> row totals tot[i].
+__global__ void k_row_scan(uint32_t *cnt, uint32_t nb, uint32_t nseg, unsigned long long *tot) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    for (uint64_t i = wid; i < nb; i += nwarps) {
+        uint32_t *row = cnt + i * nseg;
+        unsigned long long run = 0;
+        for (uint32_t s0 = 0; s0 < nseg; s0 += 32) {
+            const uint32_t s = s0 + lane;
+            const uint32_t x = s < nseg ? row[s] : 0;
+            uint32_t incl = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (s < nseg) row[s] = (uint32_t)run + incl - x;   // row offsets fit u32 (<= |V|)
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) tot[i] = run;
+    }
+}
+
+// scatter productive row totals into the per-candidate count array
+__global__ void k_scatter_counts(const unsigned long long *tot, const uint32_t *pidx, uint64_t b0, uint32_t nb,
+                                 unsigned long long *cand_cnt) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x)
+        cand_cnt[pidx[b0 + i]] = tot[i];
+}
+
+__global__ void k_fill_eps(unsigned long long *cand_cnt, uint64_t n, unsigned long long val) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+        cand_cnt[j] = val;
+}
+
+// Write sorted (src, dst) pairs: same traversal as k_tile_counts; lane b
+// keeps the running output position of source w*64+b (and +32).
+__global__ void k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
+                              uint32_t nw, uint32_t nb, uint32_t nseg, const uint32_t *cnt_scan,
+                              const uint32_t *cand, const uint32_t *pidx, uint64_t b0,
+                              const unsigned long long *start, uint64_t jlo, uint32_t *osrc, uint32_t *odst) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwg = (nw + 3) / 4;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    for (uint64_t task = wid; task < (uint64_t)nseg * nwg; task += nwarps) {
+        const uint32_t seg = (uint32_t)(task / nwg);
+        const uint32_t w0 = (uint32_t)(task % nwg) * 4;
+        unsigned long long pos[8];
+        uint32_t sid[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t i = (w0 + k / 2) * 64 + lane + 32 * (k & 1);
+            if (i < nb) {
+                const uint32_t j = pidx[b0 + i];
+                pos[k] = start[j - jlo] + cnt_scan[(uint64_t)i * nseg + seg];
+                sid[k] = cand[j];
+            } else {
+                pos[k] = 0;
+                sid[k] = 0;
+            }
+        }
+        const uint64_t vbeg = (uint64_t)seg * TILE_V, vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
+        for (uint64_t v0 = vbeg; v0 < vend; v0 += 32) {
+            const uint64_t vv = v0 + lane;
+            const uint32_t vid = vlo + (uint32_t)vv;
+            uint64_t x[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                x[k] = (vv < vend && w0 + k < nw) ? ans_word(A, S, Vis, vid, w0 + k, nw) : 0ull;
+            const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (!__ballot_sync(0xffffffffu, x[k] != 0)) continue;
+#pragma unroll 4
+                for (int b = 0; b < 64; ++b) {
+                    const bool has = (x[k] >> b) & 1ull;
+                    const unsigned m = __ballot_sync(0xffffffffu, has);
+                    if (!m) continue;
+                    const int h = b >> 5, bl = b & 31;
+                    const unsigned long long p0 = __shfl_sync(0xffffffffu, pos[2 * k + h], bl);
+                    const uint32_t s = __shfl_sync(0xffffffffu, sid[2 * k + h], bl);
+                    if (has) {
+                        const unsigned long long o = p0 + __popc(m & lt);
+                        osrc[o] = s;
+                        odst[o] = vid;
+                    }
+                    if (lane == bl) pos[2 * k + h] += __popc(m);
+                }
+            }
+        }
+    }
+}
+
+// epsilon pairs (v, v) of non-productive candidates in [jlo, jhi)
+__global__ void k_write_eps(const uint8_t *flag, const uint32_t *cand, uint64_t jlo, uint64_t jhi,
+                            const unsigned long long *start, uint32_t *osrc, uint32_t *odst) {
+    for (uint64_t j = jlo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < jhi; j += (uint64_t)gridDim.x * blockDim.x) {
+        if (flag[j]) continue;
+        const unsigned long long o = start[j - jlo];
+        osrc[o] = cand[j];
+        odst[o] = cand[j];
+    }
+}
+
+struct NZ {
+    __host__ __device__ bool operator()(const unsigned long long &x) const { return x != 0; }
+};
+
+inline int grid_for(uint64_t threads, int block = 256, int cap = 148 * 16) {
+    uint64_t g = (threads + block - 1) / block;
+    if (g > (uint64_t)cap) g = cap;
+    return g ? (int)g : 1;
+}
+
+// ---- host-side evaluation driver ------------------------------------------
+struct Workspace {
+    cudaStream_t s;
+    std::vector<void *> ptrs;
+    ~Workspace() { for (void *p : ptrs) dev_free(p, s); }
+    void *get(size_t bytes) {
+        void *p = dev_alloc(bytes, s);
+        if (p) ptrs.push_back(p);
+        return p;
+    }
+};
+
+struct Range { uint32_t lo, hi; bool empty() const { return lo > hi; } };
+
+Range hull(Range a, Range b) {
+    if (a.empty()) return b;
+    if (b.empty()) return a;
+    return {std::min(a.lo, b.lo), std::max(a.hi, b.hi)};
+}
+
+template <int CW>
+rpq_status run_levels(const DevAuto &A, const Layout &S, ExpandArgs P, uint64_t *F, uint64_t *Vis, Item *L0,
+                      Item *L1, uint64_t xwords, cudaStream_t s, bool stats, bool timeit, uint32_t first_items,
+                      uint32_t *h_cnt, rpq_stats *out_stats, cudaEvent_t ev0, cudaEvent_t ev1) {
+    // one level = expand (+ hub segments) then advance; the grid of expand is
+    // sized from the host-known worklist size, advance scans the bitmap X
+    uint32_t n = first_items;
+    int cur = 0;
+    uint32_t levels = 0;
+    Item *lists[2] = {L0, L1};
+    const int agrid = grid_for(xwords * 32, 256, 148 * 8);
+    while (n) {
+        P.cur_idx = cur;
+        P.cur = lists[cur];
+        const int grid = grid_for((uint64_t)n * CW);
+        const int hgrid = 148 * 4;
+        if (timeit) cudaEventRecord(ev0, s);
+        if (stats) {
+            k_expand<CW, true><<<grid, 256, 0, s>>>(A, S, P);
+            k_expand_hub<CW, true><<<hgrid, 256, 0, s>>>(A, S, P);
+        } else {
+            k_expand<CW, false><<<grid, 256, 0, s>>>(A, S, P);
+            k_expand_hub<CW, false><<<hgrid, 256, 0, s>>>(A, S, P);
+        }
+        if (timeit) cudaEventRecord(ev1, s);
+        k_advance<CW><<<agrid, 256, 0, s>>>(A, S, F, P.N, Vis, P.X, xwords, P.nw, P.nchunk, A.nq, lists[cur ^ 1],
+                                            &P.ctrl->cnt[cur ^ 1]);
+        RPQ_CUDA_TRY(cudaMemcpyAsync(h_cnt, &P.ctrl->cnt[cur ^ 1], 4, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(&P.ctrl->cnt[cur], 0, 4, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(&P.ctrl->nhub_recs, 0, 4, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        RPQ_CUDA_TRY(cudaGetLastError());
+        out_stats->expand_launches += 2;
+        out_stats->kernel_launches += 3;
+        if (timeit) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev0, ev1);
+            out_stats->expand_ms += ms;
+        }
+        ++levels;
+        n = *h_cnt;
+        cur ^= 1;
+    }
+    out_stats->levels += levels;
+    return RPQ_OK;
+}
+
+}  // namespace
+
+// Evaluate the RPQ from the sorted, distinct candidate sources cand[0..nsrc)
+// (device array).  cand == nullptr means all of V (all-pairs, reading R11).
+rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint32_t *d_cand_in, uint64_t nsrc,
+                               const rpq_eval_opts *opts_in, rpq_result **out) {
+    rpq_eval_opts o{};
+    if (opts_in) o = *opts_in;
+    if (o.mode == 0) o.mode = RPQ_COUNT;
+    const bool want_pairs = o.mode & RPQ_PAIRS;
+    const bool want_ps = (o.mode & RPQ_PER_SOURCE) || want_pairs;
+    const bool stats = o.mode & RPQ_STATS;
+    const bool timeit = o.mode & RPQ_TIME_KERNELS;
+    const uint32_t shard_count = o.shard_count ? o.shard_count : 1;
+    if (o.shard_index >= shard_count) return rpq_fail(RPQ_EINVAL, "shard_index >= shard_count");
+    if (a->vocab != g->label_names)
+        return rpq_fail(RPQ_EINVAL, "automaton was compiled against a different label vocabulary");
+    RPQ_CUDA_TRY(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)o.cuda_stream;
+    Workspace ws{s, {}};
+
+    rpq_result *res = new rpq_result();
+    res->device = g->device;
+    auto fail = [&](rpq_status st) { rpq_result_release(res); return st; };
+    cudaEvent_t evt0, evt1, e_begin, e_end;
+    cudaEventCreate(&evt0); cudaEventCreate(&evt1); cudaEventCreate(&e_begin); cudaEventCreate(&e_end);
+    struct EvGuard { cudaEvent_t *e; ~EvGuard() { for (int i = 0; i < 4; ++i) cudaEventDestroy(e[i]); } };
+    cudaEvent_t evs[4] = {evt0, evt1, e_begin, e_end};
+    EvGuard eg{evs};
+    cudaEventRecord(e_begin, s);
+    rpq_stats &ST = res->stats;
+
+    // ---- device automaton ------------------------------------------------
+    DevAuto A{};
+    A.nq = a->nq;
+    A.final_mask = a->final_mask;
+    std::vector<uint32_t> slot_label;
+    for (uint32_t q = 0; q <= a->nq; ++q) A.toff[q] = (uint16_t)a->off[q];
+    for (size_t t = 0; t < a->from.size(); ++t) {
+        uint32_t l = a->label[t];
+        auto it = std::find(slot_label.begin(), slot_label.end(), l);
+        int slot = (int)(it - slot_label.begin());
+        if (it == slot_label.end()) slot_label.push_back(l);
+        A.tslot[t] = (uint8_t)slot;
+        A.tto[t] = (uint8_t)a->to[t];
+    }
+    for (size_t k = 0; k < slot_label.size(); ++k) {
+        A.off[k] = g->csr[slot_label[k]].off;
+        A.nbr[k] = g->csr[slot_label[k]].nbr;
+    }
+
+    // ---- candidate sources and the productive subset P --------------------
+    const uint32_t *cand = d_cand_in;
+    if (!cand) {
+        nsrc = g->nv;
+        uint32_t *iota = (uint32_t *)ws.get(nsrc * 4);
+        if (!iota) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
+        k_iota<<<grid_for(nsrc), 256, 0, s>>>(iota, nsrc);
+        ST.kernel_launches++;
+        cand = iota;
+    }
+    uint8_t *flag = (uint8_t *)ws.get(std::max<uint64_t>(nsrc, 1));
+    uint32_t *pidx = (uint32_t *)ws.get(std::max<uint64_t>(nsrc, 1) * 4);
+    uint64_t *d_np = (uint64_t *)ws.get(8);
+    if (!flag || !pidx || !d_np) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
+    uint64_t np = 0;
+    if (nsrc && a->nq) {
+        k_productive<<<grid_for(nsrc), 256, 0, s>>>(A, cand, nsrc, flag);
+        ST.kernel_launches++;
+        size_t tb = 0;
+        thrust::counting_iterator<uint32_t> it(0);
+        cub::DeviceSelect::Flagged(nullptr, tb, it, flag, pidx, d_np, (int64_t)nsrc, s);
+        void *tmp = ws.get(tb);
+        if (!tmp) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory"));
+        cub::DeviceSelect::Flagged(tmp, tb, it, flag, pidx, d_np, (int64_t)nsrc, s);
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&np, d_np, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    } else if (nsrc) {
+        RPQ_CUDA_TRY(cudaMemsetAsync(flag, 0, nsrc, s));
+    }
+    ST.productive_sources = np;
+    const bool eps = a->accepts_empty;
+
+    // ---- ranges per state (hull of dst ranges of entering labels) ---------
+    std::vector<Range> in_range(a->nq, Range{1, 0});
+    for (size_t t = 0; t < a->from.size(); ++t) {
+        const LabelCSR &c = g->csr[a->label[t]];
+        in_range[a->to[t]] = hull(in_range[a->to[t]], Range{c.dst_min, c.dst_max});
+    }
+
+    // ---- batch plan -------------------------------------------------------
+    // Rows of the worst batch (q0 range = hull of all productive sources) set
+    // the word budget: 3 state arrays x 8 B + worklists/bitmaps per word.
+    uint32_t p_first = 0, p_last = 0;
+    if (np) {
+        uint32_t j0 = 0, j1 = 0;
+        RPQ_CUDA_TRY(cudaMemcpy(&j0, pidx, 4, cudaMemcpyDeviceToHost));
+        RPQ_CUDA_TRY(cudaMemcpy(&j1, pidx + np - 1, 4, cudaMemcpyDeviceToHost));
+        RPQ_CUDA_TRY(cudaMemcpy(&p_first, cand + j0, 4, cudaMemcpyDeviceToHost));
+        RPQ_CUDA_TRY(cudaMemcpy(&p_last, cand + j1, 4, cudaMemcpyDeviceToHost));
+    }
+    uint64_t R_max = 0;
+    for (uint32_t q = 0; q < a->nq; ++q) {
+        Range r = in_range[q];
+        if (q == 0 && np) r = hull(r, Range{p_first, p_last});
+        R_max += r.empty() ? 0 : (uint64_t)r.hi - r.lo + 1;
+    }
+    size_t free_b = 0, total_b = 0;
+    RPQ_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    uint64_t budget = o.hbm_budget_bytes ? o.hbm_budget_bytes : (uint64_t)(free_b * 0.9);
+    uint64_t B = o.batch_sources;
+    if (B == 0) {
+        // bytes per 64-source word column: 24 R (Vis, F, N) + lists/bitmaps
+        // (2 x 8 B per chunk of >= 1 word, worst case CW = 1) + extraction
+        const double per_word = 24.0 * R_max + 17.0 * R_max + 64.0 * 8 * 2;
+        uint64_t nw_max = per_word > 0 ? (uint64_t)(budget / per_word) : 1;
+        if (nw_max < 1) nw_max = 1;
+        B = std::min<uint64_t>(std::max<uint64_t>(np, 1), nw_max * 64);
+    }
+    B = std::max<uint64_t>(1, B);
+    uint64_t nw = (B + 63) / 64;
+    uint32_t CW = o.chunk_words;
+    if (CW == 0) { CW = 1; while (CW < 32 && CW < nw) CW <<= 1; }
+    if (CW != 1 && CW != 2 && CW != 4 && CW != 8 && CW != 16 && CW != 32)
+        return fail(rpq_fail(RPQ_EINVAL, "chunk_words must be 1,2,4,8,16 or 32"));
+    nw = (nw + CW - 1) / CW * CW;
+    const uint64_t nchunk = nw / CW;
+    const uint64_t nbatches = np ? (np + B - 1) / B : 0;
+    ST.batch_sources = (uint32_t)B;
+    ST.chunk_words = CW;
+
+    // batch boundaries: first/last productive candidate index of each batch
+    std::vector<uint32_t> bfirst(nbatches), blast(nbatches);
+    for (uint64_t b = 0; b < nbatches; ++b) {
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&bfirst[b], pidx + b * B, 4, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&blast[b], pidx + std::min<uint64_t>(np, (b + 1) * B) - 1, 4,
+                                     cudaMemcpyDeviceToHost, s));
+    }
+    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+
+    // ---- workspace ----------------------------------------------------------
+    const uint64_t words = R_max * nw;
+    ST.state_words = words;
+    const uint64_t list_cap = std::max<uint64_t>(R_max * nchunk, B);
+    const uint64_t xwords = (R_max * nchunk + 31) / 32 + 1;
+    const uint32_t hrec_cap = 1u << 22;
+    uint64_t *Vis = nullptr, *F = nullptr, *N = nullptr;
+    uint32_t *X = nullptr;
+    Item *L0 = nullptr, *L1 = nullptr;
+    Ctrl *ctrl = (Ctrl *)ws.get(sizeof(Ctrl));
+    unsigned long long *d_stats = (unsigned long long *)ws.get(NSTAT * 8 + 8);
+    unsigned long long *d_total = d_stats + NSTAT;
+    uint32_t *h_cnt = nullptr;
+    RPQ_CUDA_TRY(cudaMallocHost(&h_cnt, 16));
+    struct HostGuard { uint32_t *p; ~HostGuard() { cudaFreeHost(p); } } hg{h_cnt};
+    HubRec *hrecs = nullptr;
+    if (nbatches) {
+        Vis = (uint64_t *)ws.get(words * 8);
+        F = (uint64_t *)ws.get(words * 8);
+        N = (uint64_t *)ws.get(words * 8);
+        X = (uint32_t *)ws.get(xwords * 4);
+        L0 = (Item *)ws.get(list_cap * sizeof(Item));
+        L1 = (Item *)ws.get(list_cap * sizeof(Item));
+        hrecs = (HubRec *)ws.get((uint64_t)hrec_cap * sizeof(HubRec));
+        if (!Vis || !F || !N || !X || !L0 || !L1 || !hrecs)
+            return fail(rpq_fail(RPQ_ENOMEM, "out of device memory for B=%llu sources (%llu state words)",
+                                 (unsigned long long)B, (unsigned long long)words));
+        RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(F, 0, words * 8, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(N, 0, words * 8, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(X, 0, xwords * 4, s));
+    }
+    if (!ctrl || !d_stats) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory"));
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_stats, 0, NSTAT * 8 + 8, s));
+
+    // per-candidate counts (PER_SOURCE / PAIRS), initialised to the epsilon pair
+    unsigned long long *cand_cnt = nullptr;
+    if (want_ps) {
+        cand_cnt = (unsigned long long *)ws.get(std::max<uint64_t>(nsrc, 1) * 8);
+        if (!cand_cnt) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (counts)"));
+        k_fill_eps<<<grid_for(nsrc), 256, 0, s>>>(cand_cnt, nsrc, eps ? 1ull : 0ull);
+        ST.kernel_launches++;
+    }
+    struct Block { uint32_t *src, *dst; uint64_t n; };
+    std::vector<Block> blocks;
+    struct BlockGuard { std::vector<Block> *b; ~BlockGuard() { for (auto &x : *b) { cudaFree(x.src); cudaFree(x.dst); } } } bgd{&blocks};
+
+    uint64_t total = 0;
+    // candidate-index interval owned by batch b (non-productive candidates in
+    // it contribute their epsilon pair); one virtual batch when P is empty
+    auto jstart = [&](uint64_t b) -> uint64_t { return b == 0 ? 0 : (b < nbatches ? bfirst[b] : nsrc); };
+    const uint64_t nb_eff = std::max<uint64_t>(nbatches, 1);
+
+    for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count) {
+        const uint64_t jlo = jstart(b), jhi = (b + 1 < nb_eff) ? jstart(b + 1) : nsrc;
+        ST.batches++;
+        if (b >= nbatches) {   // virtual batch: only epsilon pairs
+            const uint64_t ne = eps ? (jhi - jlo) : 0;
+            total += ne;
+            if (want_pairs && ne) {
+                Block bl{nullptr, nullptr, ne};
+                if (cudaMalloc(&bl.src, ne * 4) != cudaSuccess || cudaMalloc(&bl.dst, ne * 4) != cudaSuccess) {
+                    cudaGetLastError();
+                    cudaFree(bl.src);
+                    return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (pairs)"));
+                }
+                blocks.push_back(bl);
+                unsigned long long *start = (unsigned long long *)ws.get(ne * 8 + 8);
+                if (!start) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                size_t tb = 0;
+                cub::DeviceScan::ExclusiveSum(nullptr, tb, cand_cnt + jlo, start, (int64_t)(jhi - jlo), s);
+                void *tmp = ws.get(tb);
+                if (!tmp) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                cub::DeviceScan::ExclusiveSum(tmp, tb, cand_cnt + jlo, start, (int64_t)(jhi - jlo), s);
+                k_write_eps<<<grid_for(jhi - jlo), 256, 0, s>>>(flag, cand, jlo, jhi, start, bl.src, bl.dst);
+                ST.kernel_launches++;
+            }
+            continue;
+        }
+        const uint64_t b0 = b * B;
+        const uint32_t nb = (uint32_t)std::min<uint64_t>(B, np - b0);
+        // layout for this batch
+        uint32_t s_first = 0, s_last = 0;
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&s_first, cand + bfirst[b], 4, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&s_last, cand + blast[b], 4, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        Layout S{};
+        uint64_t rows = 0;
+        Range fin_hull{1, 0};
+        for (uint32_t q = 0; q < a->nq; ++q) {
+            Range r = in_range[q];
+            if (q == 0) r = hull(r, Range{s_first, s_last});
+            S.row_base[q] = rows;
+            S.lo[q] = r.empty() ? 0 : r.lo;
+            S.len[q] = r.empty() ? 0 : r.hi - r.lo + 1;
+            rows += S.len[q];
+            if ((a->final_mask >> q) & 1) fin_hull = hull(fin_hull, r);
+        }
+        if (b != (uint64_t)o.shard_index) {   // visited words of the previous batch
+            RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
+        }
+        ExpandArgs P{};
+        P.F = F; P.N = N; P.Vis = Vis; P.X = X;
+        P.cur = L0; P.ctrl = ctrl; P.cur_idx = 0;
+        P.hrecs = hrecs; P.hrec_cap = hrec_cap;
+        P.nw = (uint32_t)nw; P.nchunk = (uint32_t)nchunk;
+        P.stats = d_stats;
+        rpq_status st = RPQ_OK;
+        switch (CW) {
+#define RPQ_CASE(C)                                                                                        \
+    case C:                                                                                                \
+        k_seed<C><<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, F, Vis, L0, ctrl, (uint32_t)nw);      \
+        ST.kernel_launches++;                                                                              \
+        st = run_levels<C>(A, S, P, F, Vis, L0, L1, xwords, s, stats, timeit, nb, h_cnt, &ST, evt0, evt1); \
+        break;
+            RPQ_CASE(1) RPQ_CASE(2) RPQ_CASE(4) RPQ_CASE(8) RPQ_CASE(16) RPQ_CASE(32)
+#undef RPQ_CASE
+        }
+        if (st != RPQ_OK) return fail(st);
+        // N and X are all zero again here (the last level activated nothing);
+        // F holds stale words that are never read without being rewritten.
+        // Extraction reads Vis of the final states.
+        const uint32_t vlo = fin_hull.empty() ? 0 : fin_hull.lo;
+        const uint64_t vn = fin_hull.empty() ? 0 : (uint64_t)fin_hull.hi - fin_hull.lo + 1;
+        const uint64_t eps_np = eps ? (jhi - jlo) - nb : 0;   // non-productive candidates in the interval
+        if (!want_ps) {
+            RPQ_CUDA_TRY(cudaMemsetAsync(d_total, 0, 8, s));
+            if (vn) {
+                k_count_total<<<grid_for(vn * nw), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, d_total);
+                ST.kernel_launches++;
+            }
+            unsigned long long t = 0;
+            RPQ_CUDA_TRY(cudaMemcpyAsync(&t, d_total, 8, cudaMemcpyDeviceToHost, s));
+            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+            total += t + eps_np;
+            continue;
+        }
+        const uint32_t nseg = (uint32_t)std::max<uint64_t>(1, (vn + TILE_V - 1) / TILE_V);
+        uint32_t *cnt = (uint32_t *)ws.get((uint64_t)nb * nseg * 4);
+        unsigned long long *tot = (unsigned long long *)ws.get((uint64_t)nb * 8);
+        if (!cnt || !tot) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (extraction)"));
+        RPQ_CUDA_TRY(cudaMemsetAsync(cnt, 0, (uint64_t)nb * nseg * 4, s));
+        const uint64_t tasks = (uint64_t)nseg * ((nw + 3) / 4);
+        if (vn) {
+            k_tile_counts<<<grid_for(tasks * 32), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, nb, nseg, cnt);
+            ST.kernel_launches++;
+        }
+        k_row_scan<<<grid_for((uint64_t)nb * 32), 256, 0, s>>>(cnt, nb, nseg, tot);
+        k_scatter_counts<<<grid_for(nb), 256, 0, s>>>(tot, pidx, b0, nb, cand_cnt);
+        ST.kernel_launches += 2;
+        // start offsets of every candidate in [jlo, jhi)
+        const uint64_t nj = jhi - jlo;
+        unsigned long long *start = (unsigned long long *)ws.get((nj + 1) * 8);
+        if (!start) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cand_cnt + jlo, start, (int64_t)nj, s);
+        void *tmp = ws.get(tb);
+        if (!tmp) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+        cub::DeviceScan::ExclusiveSum(tmp, tb, cand_cnt + jlo, start, (int64_t)nj, s);
+        unsigned long long last_start = 0, last_cnt = 0;
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&last_start, start + nj - 1, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&last_cnt, cand_cnt + jhi - 1, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        const uint64_t bt = last_start + last_cnt;
+        total += bt;
+        if (want_pairs && bt) {
+            Block bl{nullptr, nullptr, bt};
+            if (cudaMalloc(&bl.src, bt * 4) != cudaSuccess || cudaMalloc(&bl.dst, bt * 4) != cudaSuccess) {
+                cudaGetLastError();
+                cudaFree(bl.src);
+                return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (%llu pairs)", (unsigned long long)bt));
+            }
+            blocks.push_back(bl);
+            if (vn) {
+                k_write_pairs<<<grid_for(tasks * 32), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, nb, nseg, cnt,
+                                                                   cand, pidx, b0, start, jlo, bl.src, bl.dst);
+                ST.kernel_launches++;
+            }
+            if (eps) {
+                k_write_eps<<<grid_for(nj), 256, 0, s>>>(flag, cand, jlo, jhi, start, bl.src, bl.dst);
+                ST.kernel_launches++;
+            }
+        }
+        RPQ_CUDA_TRY(cudaGetLastError());
+    }
+
+    // ---- result assembly ---------------------------------------------------
+    res->count = total;
+    if (want_pairs) {
+        res->ncols = 2;
+        res->nrows = total;
+        if (blocks.size() == 1) {
+            res->cols[0] = blocks[0].src;
+            res->cols[1] = blocks[0].dst;
+            blocks.clear();
+        } else {
+            if (cudaMalloc(&res->cols[0], std::max<uint64_t>(total, 1) * 4) != cudaSuccess ||
+                cudaMalloc(&res->cols[1], std::max<uint64_t>(total, 1) * 4) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (pairs)"));
+            }
+            uint64_t off = 0;
+            for (auto &bl : blocks) {
+                RPQ_CUDA_TRY(cudaMemcpyAsync(res->cols[0] + off, bl.src, bl.n * 4, cudaMemcpyDeviceToDevice, s));
+                RPQ_CUDA_TRY(cudaMemcpyAsync(res->cols[1] + off, bl.dst, bl.n * 4, cudaMemcpyDeviceToDevice, s));
+                off += bl.n;
+            }
+        }
+    }
+    if (want_ps && nsrc) {
+        // non-zero (source, count) of this shard's batches, ascending source.
+        // Candidates of other shards' batches are zeroed first.
+        std::vector<std::pair<uint64_t, uint64_t>> foreign;
+        for (uint64_t b = 0; b < nb_eff; ++b)
+            if (b % shard_count != o.shard_index) {
+                uint64_t jl = jstart(b), jh = (b + 1 < nb_eff) ? jstart(b + 1) : nsrc;
+                if (jh > jl) RPQ_CUDA_TRY(cudaMemsetAsync(cand_cnt + jl, 0, (jh - jl) * 8, s));
+            }
+        uint8_t *nz = (uint8_t *)ws.get(nsrc);
+        uint64_t *d_n = (uint64_t *)ws.get(8);
+        if (!nz || !d_n) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+        if (cudaMalloc(&res->ps_src, nsrc * 4) != cudaSuccess || cudaMalloc(&res->ps_cnt, nsrc * 8) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+        }
+        size_t tb1 = 0, tb2 = 0;
+        cub::DeviceSelect::If(nullptr, tb1, cand_cnt, (unsigned long long *)res->ps_cnt, d_n, (int64_t)nsrc, NZ(), s);
+        cub::DeviceSelect::FlaggedIf(nullptr, tb2, cand, cand_cnt, res->ps_src, d_n, (int64_t)nsrc, NZ(), s);
+        void *tmp = ws.get(std::max(tb1, tb2));
+        if (!tmp) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+        cub::DeviceSelect::If(tmp, tb1, cand_cnt, (unsigned long long *)res->ps_cnt, d_n, (int64_t)nsrc, NZ(), s);
+        cub::DeviceSelect::FlaggedIf(tmp, tb2, cand, cand_cnt, res->ps_src, d_n, (int64_t)nsrc, NZ(), s);
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&res->n_ps, d_n, 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (stats) {
+        unsigned long long hs[NSTAT];
+        RPQ_CUDA_TRY(cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        ST.product_edges = hs[S_PE];
+        ST.word_items = hs[S_WORD_ITEMS];
+        ST.word_edge_ops = hs[S_WORD_EDGE];
+        ST.items = hs[S_ITEMS];
+        ST.item_edges = hs[S_ITEM_EDGES];
+        ST.item_transitions = hs[S_ITEM_TRANS];
+        ST.activations = hs[S_X_RED];
+        ST.next_reds = hs[S_N_RED];
+    }
+    cudaEventRecord(e_end, s);
+    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    float tms = 0;
+    cudaEventElapsedTime(&tms, e_begin, e_end);
+    ST.total_ms = tms;
+    RPQ_CUDA_TRY(cudaGetLastError());
+    *out = res;
+    return RPQ_OK;
+}
+
+// ---- public entry points ----------------------------------------------------
+static rpq_status check_common(const rpq_graph *g, const rpq_nfa *a, rpq_result **out) {
+    if (out) *out = nullptr;
+    if (!g || !a || !out) return rpq_fail(RPQ_EINVAL, "NULL argument");
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_eval_allpairs(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
+                                        rpq_result **out) {
+    rpq_status st = check_common(g, a, out);
+    if (st) return st;
+    return eval_sources_device(g, a, nullptr, 0, opts, out);
+}
+
+extern "C" rpq_status rpq_eval_sources(const rpq_graph *g, const rpq_nfa *a, const uint32_t *srcs, uint64_t n,
+                                       const rpq_eval_opts *opts, rpq_result **out) {
+    rpq_status st = check_common(g, a, out);
+    if (st) return st;
+    if (n && !srcs) return rpq_fail(RPQ_EINVAL, "NULL sources");
+    std::vector<uint32_t> v(srcs, srcs + n);
+    std::sort(v.begin(), v.end());
+    for (uint64_t i = 0; i < n; ++i) {
+        if (v[i] >= g->nv) return rpq_fail(RPQ_EINVAL, "source %u >= |V| = %u", v[i], g->nv);
+        if (i && v[i] == v[i - 1]) return rpq_fail(RPQ_EINVAL, "duplicate source %u", v[i]);
+    }
+    RPQ_CUDA_TRY(cudaSetDevice(g->device));
+    cudaStream_t s = opts ? (cudaStream_t)opts->cuda_stream : nullptr;
+    uint32_t *d = (uint32_t *)dev_alloc(std::max<uint64_t>(n, 1) * 4, s);
+    if (!d) return rpq_fail(RPQ_ENOMEM, "out of device memory");
+    if (n) {
+        cudaError_t e = cudaMemcpyAsync(d, v.data(), n * 4, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) { dev_free(d, s); return rpq_fail(RPQ_ECUDA, "%s", cudaGetErrorString(e)); }
+    }
+    st = eval_sources_device(g, a, d, n, opts, out);
+    dev_free(d, s);
+    return st;
+}
+
+extern "C" rpq_status rpq_eval_single_source(const rpq_graph *g, const rpq_nfa *a, uint32_t src,
+                                             const rpq_eval_opts *opts, rpq_result **out) {
+    rpq_status st = check_common(g, a, out);
+    if (st) return st;
+    if (src >= g->nv) return rpq_fail(RPQ_EINVAL, "source %u >= |V| = %u", src, g->nv);
+    return rpq_eval_sources(g, a, &src, 1, opts, out);
+}

@@ -1,0 +1,228 @@
+// rpq_graph_load: host (src, dst, label) triples -> per-label device CSR.
+//
+// PAPER.md: G = (V, E, L) with labelled edges; LGF keeps "a
+// separate grid ... for each edge label" so that traversal by edge label is
+// direct.  Here that becomes one CSR per label (no grid,
+// block or slice partitioning: the graphs fit in 180 GB of HBM).  E is a set
+// of (u, l, w) triples (reading R4): duplicates are removed on the device.
+//
+// Build (one-time, excluded from query time as the paper excludes loading,
+// P:1151): validate -> per-label counting scatter of 64-bit keys (u<<32|w)
+// -> per-label radix sort (CUB) -> unique -> degree histogram + scan ->
+// neighbour array.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include "internal.h"
+
+namespace {
+
+__global__ void k_validate(const uint32_t *src, const uint32_t *dst, const uint16_t *lab, uint64_t ne,
+                           uint32_t nv, uint32_t nl, int *bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne; i += (uint64_t)gridDim.x * blockDim.x)
+        if (src[i] >= nv || dst[i] >= nv || lab[i] >= nl) *bad = 1;
+}
+
+__global__ void k_label_hist(const uint16_t *lab, uint64_t ne, unsigned long long *cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t l = lab[i];
+        // warp-aggregated increment: lanes with the same label elect a leader
+        unsigned peers = __match_any_sync(__activemask(), l);
+        int leader = __ffs(peers) - 1;
+        if ((int)(threadIdx.x & 31) == leader) atomicAdd(&cnt[l], (unsigned long long)__popc(peers));
+    }
+}
+
+__global__ void k_scatter(const uint32_t *src, const uint32_t *dst, const uint16_t *lab, uint64_t ne,
+                          unsigned long long *cursor, uint64_t *keys) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t l = lab[i];
+        unsigned peers = __match_any_sync(__activemask(), l);
+        int leader = __ffs(peers) - 1;
+        int lane = threadIdx.x & 31;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&cursor[l], (unsigned long long)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        uint64_t pos = base + __popc(peers & ((1u << lane) - 1));
+        keys[pos] = ((uint64_t)src[i] << 32) | dst[i];
+    }
+}
+
+__global__ void k_degree_nbr(const uint64_t *keys, uint64_t m, uint32_t *deg, uint32_t *nbr) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        nbr[i] = (uint32_t)k;
+        atomicAdd(&deg[(k >> 32) + 1], 1u);
+    }
+}
+
+inline int grid_for(uint64_t n, int block = 256) {
+    uint64_t g = (n + block - 1) / block;
+    if (g > 148ull * 32) g = 148ull * 32;
+    if (g == 0) g = 1;
+    return (int)g;
+}
+
+struct Cleanup {
+    std::vector<void *> ptrs;
+    cudaStream_t s;
+    ~Cleanup() { for (void *p : ptrs) dev_free(p, s); }
+};
+
+}  // namespace
+
+extern "C" void rpq_graph_free(rpq_graph *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    for (auto &c : g->csr) { cudaFree(c.off); cudaFree(c.nbr); }
+    if (g->vlabel) cudaFree(g->vlabel);
+    delete g;
+}
+
+extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
+    if (out) *out = nullptr;
+    if (!d || !out) return rpq_fail(RPQ_EINVAL, "rpq_graph_load: NULL argument");
+    if (d->num_vertices == 0) return rpq_fail(RPQ_EINVAL, "rpq_graph_load: num_vertices == 0");
+    if (d->num_edges && (!d->src || !d->dst || !d->label))
+        return rpq_fail(RPQ_EINVAL, "rpq_graph_load: NULL edge arrays");
+    if (d->num_labels == 0 || d->num_labels > 65535 || !d->label_names)
+        return rpq_fail(RPQ_EINVAL, "rpq_graph_load: bad label vocabulary");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return rpq_fail(RPQ_ECUDA, "rpq_graph_load: no CUDA device");
+    }
+    if (d->device < 0 || d->device >= ndev) return rpq_fail(RPQ_EINVAL, "rpq_graph_load: bad device");
+    RPQ_CUDA_TRY(cudaSetDevice(d->device));
+    cudaStream_t s = (cudaStream_t)d->cuda_stream;
+    const uint64_t ne = d->num_edges;
+    const uint32_t nv = d->num_vertices, nl = d->num_labels;
+
+    Cleanup tmp{{}, s};
+    auto alloc = [&](size_t bytes) { void *p = dev_alloc(bytes, s); if (p) tmp.ptrs.push_back(p); return p; };
+
+    uint32_t *d_src = (uint32_t *)alloc(ne * 4), *d_dst = (uint32_t *)alloc(ne * 4);
+    uint16_t *d_lab = (uint16_t *)alloc(ne * 2);
+    int *d_bad = (int *)alloc(sizeof(int));
+    unsigned long long *d_cnt = (unsigned long long *)alloc(nl * 8ull);
+    uint64_t *keys = (uint64_t *)alloc(ne * 8), *keys2 = (uint64_t *)alloc(ne * 8);
+    uint64_t *d_nsel = (uint64_t *)alloc(8);
+    if (!d_src || !d_dst || !d_lab || !d_bad || !d_cnt || !keys || !keys2 || !d_nsel)
+        return rpq_fail(RPQ_ENOMEM, "rpq_graph_load: out of device memory");
+    if (ne) {
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_src, d->src, ne * 4, cudaMemcpyHostToDevice, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_dst, d->dst, ne * 4, cudaMemcpyHostToDevice, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_lab, d->label, ne * 2, cudaMemcpyHostToDevice, s));
+    }
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_cnt, 0, nl * 8ull, s));
+    if (ne) {
+        k_validate<<<grid_for(ne), 256, 0, s>>>(d_src, d_dst, d_lab, ne, nv, nl, d_bad);
+        k_label_hist<<<grid_for(ne), 256, 0, s>>>(d_lab, ne, d_cnt);
+    }
+    int bad = 0;
+    std::vector<unsigned long long> cnt(nl);
+    RPQ_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    RPQ_CUDA_TRY(cudaMemcpyAsync(cnt.data(), d_cnt, nl * 8ull, cudaMemcpyDeviceToHost, s));
+    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    if (bad) return rpq_fail(RPQ_EINVAL, "rpq_graph_load: vertex id >= num_vertices or label >= num_labels");
+    std::vector<unsigned long long> start(nl + 1, 0);
+    for (uint32_t l = 0; l < nl; ++l) start[l + 1] = start[l] + cnt[l];
+    RPQ_CUDA_TRY(cudaMemcpyAsync(d_cnt, start.data(), nl * 8ull, cudaMemcpyHostToDevice, s));
+    if (ne) k_scatter<<<grid_for(ne), 256, 0, s>>>(d_src, d_dst, d_lab, ne, d_cnt, keys);
+    RPQ_CUDA_TRY(cudaGetLastError());
+
+    rpq_graph *g = new rpq_graph();
+    g->device = d->device;
+    g->nv = nv;
+    for (uint32_t l = 0; l < nl; ++l) g->label_names.emplace_back(d->label_names[l] ? d->label_names[l] : "");
+    g->csr.resize(nl);
+    int vbits = 1;
+    while (vbits < 32 && (1ull << vbits) < nv) ++vbits;
+    auto fail = [&](rpq_status st, const char *m) { rpq_graph_free(g); return rpq_fail(st, "rpq_graph_load: %s", m); };
+
+    for (uint32_t l = 0; l < nl; ++l) {
+        LabelCSR &c = g->csr[l];
+        uint64_t n = cnt[l];
+        c.off = nullptr;
+        if (cudaMalloc(&c.off, (nv + 1ull) * 4) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "CSR offsets"); }
+        RPQ_CUDA_TRY(cudaMemsetAsync(c.off, 0, (nv + 1ull) * 4, s));
+        if (n == 0) {
+            if (cudaMalloc(&c.nbr, 16) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "CSR"); }
+            continue;
+        }
+        uint64_t *kin = keys + start[l], *kout = keys2 + start[l];
+        size_t tbytes = 0, t2 = 0, t3 = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tbytes, kin, kout, (int64_t)n, 0, 32 + vbits, s);
+        cub::DeviceSelect::Unique(nullptr, t2, kout, kin, d_nsel, (int64_t)n, s);
+        tbytes = std::max(tbytes, t2);
+        void *tstore = dev_alloc(tbytes, s);
+        if (!tstore) return fail(RPQ_ENOMEM, "sort temp");
+        cub::DeviceRadixSort::SortKeys(tstore, tbytes, kin, kout, (int64_t)n, 0, 32 + vbits, s);
+        cub::DeviceSelect::Unique(tstore, tbytes, kout, kin, d_nsel, (int64_t)n, s);
+        dev_free(tstore, s);
+        uint64_t m = 0;
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&m, d_nsel, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        c.m = m;
+        if (cudaMalloc(&c.nbr, std::max<uint64_t>(m, 4) * 4) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "CSR nbr"); }
+        k_degree_nbr<<<grid_for(m), 256, 0, s>>>(kin, m, c.off, c.nbr);
+        cub::DeviceScan::InclusiveSum(nullptr, t3, c.off, c.off, (int64_t)nv + 1, s);
+        void *ts = dev_alloc(t3, s);
+        if (!ts) return fail(RPQ_ENOMEM, "scan temp");
+        cub::DeviceScan::InclusiveSum(ts, t3, c.off, c.off, (int64_t)nv + 1, s);
+        dev_free(ts, s);
+        // source range from the sorted keys, destination range by reduction
+        uint64_t kfirst = 0, klast = 0;
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&kfirst, kin, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&klast, kin + m - 1, 8, cudaMemcpyDeviceToHost, s));
+        uint32_t *d_mm = (uint32_t *)dev_alloc(8, s);
+        size_t t4 = 0, t5 = 0;
+        cub::DeviceReduce::Min(nullptr, t4, c.nbr, d_mm, (int64_t)m, s);
+        cub::DeviceReduce::Max(nullptr, t5, c.nbr, d_mm + 1, (int64_t)m, s);
+        void *tr = dev_alloc(std::max(t4, t5), s);
+        if (!d_mm || !tr) return fail(RPQ_ENOMEM, "reduce temp");
+        cub::DeviceReduce::Min(tr, t4, c.nbr, d_mm, (int64_t)m, s);
+        cub::DeviceReduce::Max(tr, t5, c.nbr, d_mm + 1, (int64_t)m, s);
+        uint32_t mm[2];
+        RPQ_CUDA_TRY(cudaMemcpyAsync(mm, d_mm, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        dev_free(tr, s);
+        dev_free(d_mm, s);
+        c.src_min = (uint32_t)(kfirst >> 32);
+        c.src_max = (uint32_t)(klast >> 32);
+        c.dst_min = mm[0];
+        c.dst_max = mm[1];
+        g->ne += m;
+    }
+    if (d->vertex_label) {
+        if (d->num_vertex_labels && d->vertex_label_names)
+            for (uint32_t i = 0; i < d->num_vertex_labels; ++i)
+                g->vlabel_names.emplace_back(d->vertex_label_names[i] ? d->vertex_label_names[i] : "");
+        g->h_vlabel.assign(d->vertex_label, d->vertex_label + nv);
+        if (cudaMalloc(&g->vlabel, nv * 2ull) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "vertex labels"); }
+        RPQ_CUDA_TRY(cudaMemcpyAsync(g->vlabel, d->vertex_label, nv * 2ull, cudaMemcpyHostToDevice, s));
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(RPQ_ECUDA, cudaGetErrorString(e));
+    *out = g;
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_graph_info(const rpq_graph *g, uint32_t *nv, uint64_t *ne, uint32_t *nl) {
+    if (!g) return rpq_fail(RPQ_EINVAL, "NULL graph");
+    if (nv) *nv = g->nv;
+    if (ne) *ne = g->ne;
+    if (nl) *nl = (uint32_t)g->csr.size();
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_graph_label_csr(const rpq_graph *g, uint32_t l, const uint32_t **off,
+                                          const uint32_t **nbr, uint64_t *m) {
+    if (!g || l >= g->csr.size()) return rpq_fail(RPQ_EINVAL, "bad graph/label");
+    if (off) *off = g->csr[l].off;
+    if (nbr) *nbr = g->csr[l].nbr;
+    if (m) *m = g->csr[l].m;
+    return RPQ_OK;
+}

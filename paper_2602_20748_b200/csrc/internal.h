@@ -1,0 +1,83 @@
+// Internal structures of the C-ABI library (not part of the ABI).
+// PAPER.md citations as "P:n" (/root/reference/PAPER.md line n).
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "rpq.h"
+
+// ---- error reporting (thread-local message, rpq_last_error) --------------
+rpq_status rpq_fail(rpq_status st, const char *fmt, ...);
+void rpq_clear_error();
+
+// ---- graph: per-label CSR ("a separate grid for each edge label") --
+struct LabelCSR {
+    uint32_t *off = nullptr;     // device [nv + 1]
+    uint32_t *nbr = nullptr;     // device [m], ascending per row
+    uint64_t m = 0;              // distinct edges with this label
+    uint32_t src_min = 1, src_max = 0;   // empty label: min > max
+    uint32_t dst_min = 1, dst_max = 0;
+};
+
+struct rpq_graph {
+    int device = 0;
+    uint32_t nv = 0;
+    uint64_t ne = 0;             // distinct (u,l,w) triples (reading R4)
+    std::vector<std::string> label_names;
+    std::vector<std::string> vlabel_names;
+    std::vector<LabelCSR> csr;   // [num_labels]
+    uint16_t *vlabel = nullptr;  // device [nv] or null
+    std::vector<uint16_t> h_vlabel;   // host copy (CRPQ planning)
+};
+
+// ---- automaton ("automata plan") ------------------------------
+struct rpq_nfa {
+    uint32_t nq = 0;                 // states; 0 is initial
+    uint64_t final_mask = 0;         // bit q set => q final
+    bool accepts_empty = false;      // initial state final (epsilon in L)
+    bool is_dfa = true;
+    std::vector<uint32_t> from, label, to;   // sorted by (from, label, to)
+    std::vector<uint32_t> off;       // [nq + 1] transitions of state q: off[q]..off[q+1]
+    uint32_t vocab_size = 0;
+    std::vector<std::string> vocab;  // label names the ids refer to
+};
+
+// ---- result --------------------------------------------------------------
+struct rpq_result {
+    int device = 0;
+    uint32_t ncols = 0;
+    uint64_t nrows = 0;              // rows materialised (PAIRS / CRPQ)
+    uint32_t *cols[RPQ_MAX_COLS] = {};   // device column buffers
+    uint64_t count = 0;              // result size (also in COUNT-only mode)
+    // RPQ_PER_SOURCE: non-zero (source, count), ascending source (device)
+    uint32_t *ps_src = nullptr;
+    uint64_t *ps_cnt = nullptr;
+    uint64_t n_ps = 0;
+    rpq_stats stats{};
+};
+
+// ---- device memory (stream-ordered pool allocator) -----------------------
+void *dev_alloc(size_t bytes, void *stream);          // nullptr on failure
+void dev_free(void *p, void *stream);
+void rpq_result_release(rpq_result *r);
+
+// ---- evaluation driver (eval.cu) -----------------------------------------
+// sources: device, sorted ascending, distinct, < nv (nullptr => all of V)
+rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint32_t *d_sources,
+                               uint64_t nsrc, const rpq_eval_opts *opts, rpq_result **out);
+
+// ---- compile (regex.cpp) -------------------------------------------------
+rpq_status compile_regex(const std::vector<std::string> &vocab, const char *regex, uint32_t flags,
+                         rpq_nfa **out, size_t *err_offset);
+
+#define RPQ_CUDA_TRY(expr)                                                              \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return rpq_fail(_e == cudaErrorMemoryAllocation ? RPQ_ENOMEM : RPQ_ECUDA,  \
+                            "%s:%d %s: %s", __FILE__, __LINE__, #expr,                  \
+                            cudaGetErrorString(_e));                                    \
+    } while (0)
