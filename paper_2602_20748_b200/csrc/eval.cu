@@ -51,6 +51,10 @@ constexpr int MAXL = RPQ_MAX_QUERY_LABELS;
 constexpr uint32_t HUB_EDGES = 512;      // edges per hub segment
 constexpr int TILE_V = 1024;             // vertices per extraction tile
 constexpr int NSTAT = 8;
+#ifndef RPQ_LEVEL_MINB
+#define RPQ_LEVEL_MINB 2
+#endif
+constexpr int KGRP = 8;                 // chunks of a row advanced/expanded together
 
 struct DevAuto {
     uint32_t nq;
@@ -68,34 +72,44 @@ struct Layout {
     uint32_t len[MAXQ];
 };
 
-struct Item {
-    uint32_t v;
-    uint32_t qc;               // q << 24 | chunk
+struct HubItem {                // a deferred row-group (frontier words in hubF)
+    uint32_t row;              // global row (state, vertex)
+    uint32_t xw;               // X word of the row (chunk block of 32)
+    uint32_t nk;               // active chunks in the group (<= KGRP)
+    uint64_t bits;             // chunk positions within the X word, 8 bits each
 };
 
 struct HubRec {                // one HUB_EDGES-edge segment of a long CSR row
-    uint32_t v, qc;            // item
+    uint32_t hitem;
     uint32_t t;                // automaton transition
     uint32_t beg, end;         // CSR edge range
 };
 
-struct Ctrl {                  // per-level counters (device)
-    uint32_t cnt[2];           // worklist sizes (ping-pong)
+struct Ctrl {                  // per-level device counters / flags
+    uint32_t active[2];        // "some row was activated" flag per level parity
+    uint32_t nhub_items;
     uint32_t nhub_recs;
-    uint32_t pad;
 };
 
-struct ExpandArgs {
-    const uint64_t *F;         // frontier words (read-only during expand)
-    uint64_t *N;               // next-frontier accumulator (red.or targets)
-    const uint64_t *Vis;       // visited words (read-only during expand)
-    uint32_t *X;               // activity bitmap over (row, chunk)
-    const Item *cur;
+// One BFS level over the rows whose activity bit is set in (Xcur, XBcur).
+//   row r = (state q, vertex v); word (r, col) holds 64 sources' bits.
+//   X word (r, xw) = which 32-word chunks of the row are active;
+//   XB bit (xi / 32) = some X word in [32 (xi/32), +32) is non-zero.
+struct LevelArgs {
+    uint64_t *N;               // next-frontier accumulator (red.or / exch)
+    uint64_t *Vis;             // visited (written only by the row's owner)
+    uint32_t *Xcur, *Xnext;    // chunk-activity bitmaps, one word per (row, xw)
+    uint32_t *XBcur, *XBnext;  // block bitmaps: one bit per 32 X words
+    uint64_t nxwords;          // rows * nxw
     Ctrl *ctrl;
-    int cur_idx;               // ctrl->cnt[cur_idx] = items in cur
+    int par;                   // level parity
+    HubItem *hitems;
+    uint64_t *hubF;            // [hitem][KGRP][32] frontier words
     HubRec *hrecs;
-    uint32_t hrec_cap;
-    uint32_t nw, nchunk;
+    uint32_t hitem_cap, hrec_cap;
+    uint32_t nw;               // words per row
+    uint32_t nxw;              // X words per row
+    uint32_t cw;               // words per chunk (power of two <= 32)
     unsigned long long *stats;
 };
 
@@ -104,236 +118,259 @@ enum { S_PE = 0, S_WORD_ITEMS, S_WORD_EDGE, S_ITEMS, S_ITEM_EDGES, S_ITEM_TRANS,
 
 __device__ __forceinline__ uint64_t ld_cg(const uint64_t *p) { return __ldcg((const unsigned long long *)p); }
 
-// fire-and-forget OR into global memory (RED.E.OR.64: no return value, so
-// the issuing warp never waits for the L2 round trip)
+// fire-and-forget reductions (RED: no return value, the warp never waits)
 __device__ __forceinline__ void red_or64(uint64_t *p, uint64_t v) {
     asm volatile("red.relaxed.gpu.global.or.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void red_or32(uint32_t *p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_and32(uint32_t *p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
-// Expand one (item, transition) over CSR edges [beg, end) for a group of CW
-// lanes; f is this lane's frontier word.  Per target row: m = f & ~Vis;
-// N |= m (red.or); mark (row, chunk) active in X (test, then red.or).
-template <int CW, bool STATS>
-__device__ __forceinline__ void expand_edges(const ExpandArgs &p, const DevAuto &A, const Layout &S, int t,
-                                             uint32_t beg, uint32_t end, uint64_t f, uint32_t c,
-                                             unsigned gmask, int gl, unsigned long long *st) {
-    const int slot = A.tslot[t];
-    const uint32_t q2 = A.tto[t];
-    const uint32_t *__restrict__ nbr = A.nbr[slot];
-    const uint64_t tbase = S.row_base[q2] - S.lo[q2];
-    const uint64_t col = (uint64_t)c * CW + gl;
-    const int fpop = __popcll(f);
-    constexpr int R = CW >= 8 ? 1 : 8 / CW;   // neighbour ids held per lane
-    constexpr int EPI = CW * R;               // edges per iteration (multiple of 8)
-    for (uint32_t j = beg; j < end; j += EPI) {
-        uint32_t mine[R];
+__device__ __forceinline__ int row_state(const Layout &S, uint32_t nq, uint64_t row) {
+    int q = 0;
+    while (q + 1 < (int)nq && S.row_base[q + 1] <= row) ++q;
+    return q;
+}
+
+// Expand the edges [beg, end) of one CSR row for a group of up to KGRP
+// active chunks of X word xw (chunk positions packed 8 bits each in `bits`).
+// KC chunks x (8 / KC) edges are in flight per step, so every lane keeps 8
+// independent visited-word loads outstanding.
+//   m = f & ~Vis[t];  N[t] |= m (red);  X/XB activity of t (test, red).
+template <int KC, bool STATS>
+__device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S, uint32_t q2,
+                                             const uint32_t *__restrict__ nbr, uint32_t beg, uint32_t end,
+                                             const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
+                                             unsigned long long *st) {
+    constexpr int E = KGRP / KC;
+    const uint32_t tbase = (uint32_t)(S.row_base[q2] - S.lo[q2]);
+    const uint32_t colbase = xw * 32u * p.cw + lane;
+    int fpop = 0, nzw = 0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            uint32_t idx = j + r * CW + gl;
-            mine[r] = idx < end ? __ldg(nbr + idx) : 0u;
-        }
-        const int cnt = (int)((end - j) < (uint32_t)EPI ? (end - j) : (uint32_t)EPI);
-        for (int k0 = 0; k0 < cnt; k0 += 8) {
-            uint64_t trow[8], vis[8];
-            uint32_t xw[8];
-            // issue all loads of the 8 targets before any dependent work
+    for (int k = 0; k < KC; ++k) { fpop += __popcll(f[k]); nzw += f[k] != 0; }
+    for (uint32_t j = beg; j < end; j += 32) {
+        const uint32_t my = (j + lane < end) ? __ldg(nbr + j + lane) : 0u;
+        const int cnt = (int)((end - j) < 32u ? (end - j) : 32u);
+        for (int e0 = 0; e0 < cnt; e0 += E) {
+            uint32_t trow[E], xo[E];
+            uint64_t vis[E][KC];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int k = k0 + u;
-                uint32_t w;
-                if constexpr (CW >= 8) w = __shfl_sync(gmask, mine[0], k & (CW - 1), CW);
-                else w = __shfl_sync(gmask, mine[(u / CW) % R], u % CW, CW);
-                trow[u] = tbase + w;
-                vis[u] = (f && k < cnt) ? __ldg((const unsigned long long *)(p.Vis + trow[u] * p.nw + col)) : ~0ull;
-                const uint64_t bi = trow[u] * p.nchunk + c;
-                xw[u] = (gl == 0 && k < cnt) ? __ldcg(p.X + (bi >> 5)) : ~0u;
-            }
+            for (int e = 0; e < E; ++e) {
+                const bool ok = e0 + e < cnt;
+                trow[e] = tbase + __shfl_sync(0xffffffffu, my, (e0 + e) & 31);
+                const uint64_t rb = (uint64_t)trow[e] * p.nw + colbase;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint64_t m = f & ~vis[u];
-                if (m) red_or64(p.N + trow[u] * p.nw + col, m);
-                const unsigned am = __ballot_sync(gmask, m != 0) & gmask;
-                if (am && gl == 0) {
-                    const uint64_t bi = trow[u] * p.nchunk + c;
-                    const uint32_t bit = 1u << (bi & 31);
-                    if (!(xw[u] & bit)) {
-                        red_or32(p.X + (bi >> 5), bit);
-                        if (STATS) st[S_X_RED]++;
-                    }
+                for (int k = 0; k < KC; ++k) {
+                    const uint32_t ck = (uint32_t)(bits >> (8 * k)) & 0xffu;
+                    vis[e][k] = (ok && f[k]) ? ld_cg(p.Vis + rb + ck * p.cw) : ~0ull;
                 }
-                if (STATS && m) st[S_N_RED]++;
+                xo[e] = (lane == 0 && ok) ? __ldcg(p.Xnext + (uint64_t)trow[e] * p.nxw + xw) : ~0u;
+            }
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                uint32_t newmask = 0;
+                const uint64_t rb = (uint64_t)trow[e] * p.nw + colbase;
+#pragma unroll
+                for (int k = 0; k < KC; ++k) {
+                    const uint32_t ck = (uint32_t)(bits >> (8 * k)) & 0xffu;
+                    const uint64_t m = f[k] & ~vis[e][k];
+                    if (m) {
+                        red_or64(p.N + rb + ck * p.cw, m);
+                        if (STATS) st[S_N_RED]++;
+                    }
+                    if (__ballot_sync(0xffffffffu, m != 0)) newmask |= 1u << ck;
+                }
+                if (lane == 0 && (newmask & ~xo[e])) {
+                    const uint64_t xi = (uint64_t)trow[e] * p.nxw + xw;
+                    red_or32(p.Xnext + xi, newmask);
+                    red_or32(p.XBnext + (xi >> 10), 1u << ((xi >> 5) & 31));
+                    p.ctrl->active[p.par ^ 1] = 1u;
+                    if (STATS) st[S_X_RED]++;
+                }
             }
         }
-        if (STATS && f) {
-            st[S_WORD_EDGE] += cnt;
+        if (STATS && nzw) {
+            st[S_WORD_EDGE] += (unsigned long long)nzw * cnt;
             st[S_PE] += (unsigned long long)fpop * cnt;
         }
-        if (STATS && gl == 0) st[S_ITEM_EDGES] += cnt;
+        if (STATS && lane == 0) st[S_ITEM_EDGES] += cnt;
     }
 }
 
 template <bool STATS>
 __device__ __forceinline__ void flush_stats(unsigned long long *st, unsigned long long *out) {
-    if constexpr (!STATS) return;
-    else {
+    if constexpr (STATS) {
 #pragma unroll
-    for (int i = 0; i < NSTAT; ++i) {
-        unsigned long long x = st[i];
+        for (int i = 0; i < NSTAT; ++i) {
+            unsigned long long x = st[i];
 #pragma unroll
-        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, x);
-    }
-    }
-}
-
-template <int CW, bool STATS>
-__global__ void __launch_bounds__(256) k_expand(const DevAuto A, const Layout S, const ExpandArgs p) {
-    const int lane = threadIdx.x & 31;
-    const int gl = lane & (CW - 1);
-    const unsigned gmask = CW == 32 ? 0xffffffffu : (((1u << CW) - 1u) << (lane & ~(CW - 1)));
-    const uint64_t ngroups = (uint64_t)gridDim.x * blockDim.x / CW;
-    const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / CW;
-    const uint32_t n = p.ctrl->cnt[p.cur_idx];
-    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
-    // all lanes of a warp run the same number of outer iterations so that the
-    // final stats reduction is warp-uniform; groups past n idle.
-    const uint64_t wfirst = gid - (uint64_t)(lane / CW);
-    for (uint64_t base = wfirst; base < n; base += ngroups) {
-        const uint64_t it = base + (uint64_t)(lane / CW);
-        if (it >= n) continue;   // whole group skips together
-        const Item item = p.cur[it];
-        const uint32_t v = item.v, q = item.qc >> 24, c = item.qc & 0xffffffu;
-        const uint64_t row = S.row_base[q] + (v - S.lo[q]);
-        const uint64_t f = p.F[row * p.nw + (uint64_t)c * CW + gl];
-        if (STATS && gl == 0) st[S_ITEMS]++;
-        if (STATS && f) st[S_WORD_ITEMS]++;
-        for (int t = A.toff[q]; t < A.toff[q + 1]; ++t) {
-            const uint32_t *off = A.off[A.tslot[t]];
-            const uint32_t beg = __ldg(off + v), end = __ldg(off + v + 1);
-            if (STATS && gl == 0) st[S_ITEM_TRANS]++;
-            if (end == beg) continue;
-            if (end - beg > HUB_EDGES) {
-                // long row: one record per HUB_EDGES-edge segment, expanded by
-                // k_expand_hub (F is read-only during the level, so the hub
-                // kernel reads the frontier words itself)
-                const uint32_t nseg = (end - beg + HUB_EDGES - 1) / HUB_EDGES;
-                uint32_t r = 0;
-                if (gl == 0) r = atomicAdd(&p.ctrl->nhub_recs, nseg);
-                r = __shfl_sync(gmask, r, 0, CW);
-                if (r + nseg <= p.hrec_cap) {
-                    for (uint32_t s = gl; s < nseg; s += CW) {
-                        const uint32_t b = beg + s * HUB_EDGES;
-                        p.hrecs[r + s] = HubRec{v, item.qc, (uint32_t)t, b, min(end, b + HUB_EDGES)};
-                    }
-                    continue;
-                }
-                // overflow: neutralise the reserved records, expand inline
-                for (uint32_t s = gl; r + s < p.hrec_cap && s < nseg; s += CW)
-                    p.hrecs[r + s] = HubRec{0u, 0u, 0u, 0u, 0u};
-            }
-            expand_edges<CW, STATS>(p, A, S, t, beg, end, f, c, gmask, gl, st);
+            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            if ((threadIdx.x & 31) == 0 && x) atomicAdd(out + i, x);
         }
     }
-    flush_stats<STATS>(st, p.stats);
 }
 
-template <int CW, bool STATS>
-__global__ void __launch_bounds__(256) k_expand_hub(const DevAuto A, const Layout S, const ExpandArgs p) {
-    const int lane = threadIdx.x & 31;
-    const int gl = lane & (CW - 1);
-    const unsigned gmask = CW == 32 ? 0xffffffffu : (((1u << CW) - 1u) << (lane & ~(CW - 1)));
-    const uint64_t ngroups = (uint64_t)gridDim.x * blockDim.x / CW;
-    const uint64_t gid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) / CW;
-    const uint32_t n = min(p.ctrl->nhub_recs, p.hrec_cap);
-    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const uint64_t wfirst = gid - (uint64_t)(lane / CW);
-    for (uint64_t base = wfirst; base < n; base += ngroups) {
-        const uint64_t it = base + (uint64_t)(lane / CW);
-        if (it >= n) continue;
-        const HubRec r = p.hrecs[it];
-        if (r.end == r.beg) continue;
-        const uint32_t q = r.qc >> 24, c = r.qc & 0xffffffu;
-        const uint64_t row = S.row_base[q] + (r.v - S.lo[q]);
-        const uint64_t f = p.F[row * p.nw + (uint64_t)c * CW + gl];
-        expand_edges<CW, STATS>(p, A, S, (int)r.t, r.beg, r.end, f, c, gmask, gl, st);
-    }
-    flush_stats<STATS>(st, p.stats);
+template <bool STATS>
+__device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const Layout &S, uint32_t q2,
+                                               const uint32_t *nbr, uint32_t beg, uint32_t end,
+                                               const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
+                                               unsigned long long *st) {
+    if (nk > 4) expand_edges<8, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st);
+    else if (nk > 2) expand_edges<4, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st);
+    else if (nk > 1) expand_edges<2, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st);
+    else expand_edges<1, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st);
 }
 
-// Advance (end of a level): for every active (row, chunk) of X:
-//   n = N & ~Vis; F = n; Vis |= n; N = 0; X bit cleared;
-// and append the item to the next worklist if n != 0.  A warp takes one X
-// word (32 items); its CW-lane groups take the set bits.
-template <int CW>
-__global__ void __launch_bounds__(256) k_advance(const DevAuto A, const Layout S, uint64_t *F, uint64_t *N,
-                                                 uint64_t *Vis, uint32_t *X, uint64_t xwords, uint32_t nw,
-                                                 uint32_t nchunk, uint32_t nq, Item *next, uint32_t *next_cnt) {
-    constexpr int G = 32 / CW;
+// Main level kernel: a warp owns one active X word = one row and up to 32 of
+// its chunks; groups of KGRP active chunks are advanced (N -> Vis, fused:
+// f = exch(N, 0) & ~Vis; Vis |= f) and then expanded along every automaton
+// transition of the row's state.  Work units (32 X words = one XB bit) are
+// interleaved over warps.
+template <bool STATS>
+__global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, const Layout S, const LevelArgs p) {
     const int lane = threadIdx.x & 31;
-    const int gl = lane & (CW - 1), grp = lane / CW;
-    const unsigned gmask = CW == 32 ? 0xffffffffu : (((1u << CW) - 1u) << (lane & ~(CW - 1)));
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    for (uint64_t xi = wid; xi < xwords; xi += nwarps) {
-        uint32_t x = __ldcg(X + xi);
-        if (!x) continue;
-        if (lane == 0) X[xi] = 0;
-        // the set bits are shared out G per round
-        while (x) {
-            // group grp takes the grp-th lowest set bit of x (if any)
-            uint32_t y = x;
-            for (int k = 0; k < grp && y; ++k) y &= y - 1;
-            const bool has = y != 0;
-            const int b = has ? __ffs(y) - 1 : 0;
-            for (int k = 0; k < G && x; ++k) x &= x - 1;   // drop the bits taken this round
-            if (!has) continue;
-            const uint64_t it = xi * 32 + b;
-            const uint64_t row = it / nchunk;
-            const uint32_t c = (uint32_t)(it % nchunk);
-            const uint64_t wi = row * nw + (uint64_t)c * CW + gl;
-            uint64_t n = N[wi];
-            uint64_t vis = Vis[wi];
-            n &= ~vis;
-            F[wi] = n;
-            if (n) Vis[wi] = vis | n;
-            N[wi] = 0;
-            const unsigned any = __ballot_sync(gmask, n != 0) & gmask;
-            if (any && gl == 0) {
-                int q = 0;
-                while (q + 1 < (int)nq && S.row_base[q + 1] <= row) ++q;
-                const uint32_t v = S.lo[q] + (uint32_t)(row - S.row_base[q]);
-                cg::coalesced_group g = cg::coalesced_threads();
-                uint32_t pos = 0;
-                if (g.thread_rank() == 0) pos = atomicAdd(next_cnt, (uint32_t)g.size());
-                pos = g.shfl(pos, 0) + g.thread_rank();
-                next[pos] = Item{v, ((uint32_t)q << 24) | c};
+    const uint64_t nunits = (p.nxwords + 31) >> 5;
+    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t u = wid; u < nunits; u += nwarps) {
+        const uint32_t xb = __ldcg(p.XBcur + (u >> 5));
+        if (!((xb >> (u & 31)) & 1u)) continue;
+        if (lane == 0) red_and32(p.XBcur + (u >> 5), ~(1u << (u & 31)));
+        const uint64_t xi_l = u * 32 + lane;
+        const uint32_t xl = xi_l < p.nxwords ? __ldcg(p.Xcur + xi_l) : 0u;
+        if (xl) p.Xcur[xi_l] = 0u;
+        unsigned todo = __ballot_sync(0xffffffffu, xl != 0);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            uint32_t x = __shfl_sync(0xffffffffu, xl, src);
+            const uint64_t xi = u * 32 + src;
+            const uint64_t row = xi / p.nxw;
+            const uint32_t xw = (uint32_t)(xi % p.nxw);
+            const int q = row_state(S, A.nq, row);
+            const uint32_t v = S.lo[q] + (uint32_t)(row - S.row_base[q]);
+            const uint64_t rb = row * p.nw + xw * 32u * p.cw + lane;
+            const bool lane_ok = lane < (int)p.cw;
+            while (x) {
+                // take up to KGRP active chunks; advance N -> f (fused)
+                uint64_t f[KGRP];
+                uint64_t bits = 0;
+                int nk = 0;
+#pragma unroll
+                for (int k = 0; k < KGRP; ++k) {
+                    const bool has = x != 0;
+                    const uint32_t bt = has ? (uint32_t)(__ffs(x) - 1) : 0u;
+                    if (has) x &= x - 1;
+                    nk += has;
+                    bits |= (uint64_t)bt << (8 * k);
+                    const bool ok = has && lane_ok && xw * 32u * p.cw + bt * p.cw + lane < p.nw;
+                    f[k] = ok ? ld_cg(p.N + rb + bt * p.cw) : 0ull;
+                }
+#pragma unroll
+                for (int k = 0; k < KGRP; ++k) {
+                    const uint32_t bt = (uint32_t)(bits >> (8 * k)) & 0xffu;
+                    if (f[k]) {
+                        uint64_t *np_ = p.N + rb + bt * p.cw;
+                        const uint64_t n = atomicExch((unsigned long long *)np_, 0ull);
+                        const uint64_t vis = ld_cg(p.Vis + rb + bt * p.cw);
+                        f[k] = n & ~vis;
+                        if (f[k]) {
+                            p.Vis[rb + bt * p.cw] = vis | f[k];
+                            if (STATS) st[S_WORD_ITEMS]++;
+                        }
+                    }
+                }
+                bool anyk = false;
+#pragma unroll
+                for (int k = 0; k < KGRP; ++k) anyk |= f[k] != 0;
+                if (!__ballot_sync(0xffffffffu, anyk)) continue;
+                if (STATS && lane == 0) st[S_ITEMS]++;
+                int hslot = -1;
+                for (int t = A.toff[q]; t < A.toff[q + 1]; ++t) {
+                    const int slot = A.tslot[t];
+                    const uint32_t *off = A.off[slot];
+                    const uint32_t beg = __ldg(off + v), end = __ldg(off + v + 1);
+                    if (STATS && lane == 0) st[S_ITEM_TRANS]++;
+                    if (end == beg) continue;
+                    if (end - beg > HUB_EDGES) {
+                        if (hslot < 0) {
+                            uint32_t hs = 0;
+                            if (lane == 0) hs = atomicAdd(&p.ctrl->nhub_items, 1u);
+                            hs = __shfl_sync(0xffffffffu, hs, 0);
+                            if (hs < p.hitem_cap) {
+                                hslot = (int)hs;
+#pragma unroll
+                                for (int k = 0; k < KGRP; ++k) p.hubF[((uint64_t)hs * KGRP + k) * 32 + lane] = f[k];
+                                if (lane == 0) p.hitems[hs] = HubItem{(uint32_t)row, xw, (uint32_t)nk, bits};
+                            }
+                        }
+                        if (hslot >= 0) {
+                            const uint32_t nseg = (end - beg + HUB_EDGES - 1) / HUB_EDGES;
+                            uint32_t r = 0;
+                            if (lane == 0) r = atomicAdd(&p.ctrl->nhub_recs, nseg);
+                            r = __shfl_sync(0xffffffffu, r, 0);
+                            if (r + nseg <= p.hrec_cap) {
+                                for (uint32_t sg = lane; sg < nseg; sg += 32) {
+                                    const uint32_t b0 = beg + sg * HUB_EDGES;
+                                    p.hrecs[r + sg] = HubRec{(uint32_t)hslot, (uint32_t)t, b0, min(end, b0 + HUB_EDGES)};
+                                }
+                                continue;
+                            }
+                            for (uint32_t sg = lane; r + sg < p.hrec_cap && sg < nseg; sg += 32)
+                                p.hrecs[r + sg] = HubRec{0u, 0u, 0u, 0u};
+                        }
+                    }
+                    dispatch_edges<STATS>(nk, p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st);
+                }
             }
         }
     }
+    flush_stats<STATS>(st, p.stats);
 }
 
-// Seed batch sources: source i of the batch gets bit i in F and Vis of row
-// (q0, s_i); one item per source (rows are distinct, so no atomics).  The
-// whole CW-word chunk of F is written (F is never bulk-cleared).
-template <int CW>
+// Deferred long rows: a warp per HUB_EDGES-edge segment.
+template <bool STATS>
+__global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto A, const Layout S, const LevelArgs p) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    const uint32_t n = min(p.ctrl->nhub_recs, p.hrec_cap);
+    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (uint64_t it = wid; it < n; it += nwarps) {
+        const HubRec r = p.hrecs[it];
+        if (r.end == r.beg) continue;
+        const HubItem h = p.hitems[r.hitem];
+        uint64_t f[KGRP];
+#pragma unroll
+        for (int k = 0; k < KGRP; ++k) f[k] = p.hubF[((uint64_t)r.hitem * KGRP + k) * 32 + lane];
+        dispatch_edges<STATS>((int)h.nk, p, S, A.tto[r.t], A.nbr[A.tslot[r.t]], r.beg, r.end, f, h.bits, h.xw, lane,
+                              st);
+    }
+    flush_stats<STATS>(st, p.stats);
+}
+
+// Seed batch sources: source i of the batch gets bit i in N of row (q0, s_i)
+// and its chunk is marked active; the first level moves it into Vis.
 __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const uint32_t *__restrict__ pidx,
-                       uint64_t b0, uint32_t nb, uint64_t *F, uint64_t *Vis, Item *cur, Ctrl *ctrl, uint32_t nw) {
+                       uint64_t b0, uint32_t nb, uint64_t *N, uint32_t *X, uint32_t *XB, uint32_t nw, uint32_t nxw,
+                       uint32_t cw, Ctrl *ctrl) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
         const uint32_t s = cand[pidx[b0 + i]];
         const uint64_t row = S.row_base[0] + (s - S.lo[0]);
-        const uint32_t w = i >> 6, c = w / CW;
-        const uint64_t bit = 1ull << (i & 63);
-#pragma unroll
-        for (int k = 0; k < CW; ++k) F[row * nw + (uint64_t)c * CW + k] = (c * CW + k == w) ? bit : 0ull;
-        Vis[row * nw + w] = bit;
-        cur[i] = Item{s, (0u << 24) | c};
+        const uint32_t w = i >> 6, c = w / cw;
+        N[row * nw + w] = 1ull << (i & 63);          // rows are distinct: plain stores
+        const uint64_t xi = row * nxw + c / 32;
+        X[xi] = 1u << (c & 31);
+        atomicOr(XB + (xi >> 10), 1u << ((xi >> 5) & 31));
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ctrl->cnt[0] = nb;
-        ctrl->cnt[1] = 0;
+        ctrl->active[0] = nb ? 1u : 0u;
+        ctrl->active[1] = 0;
+        ctrl->nhub_items = 0;
         ctrl->nhub_recs = 0;
     }
 }
@@ -564,48 +601,45 @@ Range hull(Range a, Range b) {
     return {std::min(a.lo, b.lo), std::max(a.hi, b.hi)};
 }
 
-template <int CW>
-rpq_status run_levels(const DevAuto &A, const Layout &S, ExpandArgs P, uint64_t *F, uint64_t *Vis, Item *L0,
-                      Item *L1, uint64_t xwords, cudaStream_t s, bool stats, bool timeit, uint32_t first_items,
-                      uint32_t *h_cnt, rpq_stats *out_stats, cudaEvent_t ev0, cudaEvent_t ev1) {
-    // one level = expand (+ hub segments) then advance; the grid of expand is
-    // sized from the host-known worklist size, advance scans the bitmap X
-    uint32_t n = first_items;
-    int cur = 0;
+rpq_status run_levels(const DevAuto &A, const Layout &S, LevelArgs P, uint32_t *X0, uint32_t *X1, uint32_t *XB0,
+                      uint32_t *XB1, cudaStream_t s, bool stats, bool timeit, uint32_t *h_flag, rpq_stats *out_stats,
+                      cudaEvent_t ev0, cudaEvent_t ev1) {
+    // one level = k_level (+ hub segments); the host only reads a 4-byte
+    // "anything activated" flag per level
+    const uint64_t nunits = (P.nxwords + 31) / 32;
+    const int grid = grid_for(nunits * 32, 256, 148 * 3);
+    const int hgrid = 148 * 3;
+    int par = 0;
     uint32_t levels = 0;
-    Item *lists[2] = {L0, L1};
-    const int agrid = grid_for(xwords * 32, 256, 148 * 8);
-    while (n) {
-        P.cur_idx = cur;
-        P.cur = lists[cur];
-        const int grid = grid_for((uint64_t)n * CW);
-        const int hgrid = 148 * 4;
+    uint32_t *X[2] = {X0, X1}, *XB[2] = {XB0, XB1};
+    for (;;) {
+        P.par = par;
+        P.Xcur = X[par]; P.Xnext = X[par ^ 1];
+        P.XBcur = XB[par]; P.XBnext = XB[par ^ 1];
         if (timeit) cudaEventRecord(ev0, s);
         if (stats) {
-            k_expand<CW, true><<<grid, 256, 0, s>>>(A, S, P);
-            k_expand_hub<CW, true><<<hgrid, 256, 0, s>>>(A, S, P);
+            k_level<true><<<grid, 256, 0, s>>>(A, S, P);
+            k_level_hub<true><<<hgrid, 256, 0, s>>>(A, S, P);
         } else {
-            k_expand<CW, false><<<grid, 256, 0, s>>>(A, S, P);
-            k_expand_hub<CW, false><<<hgrid, 256, 0, s>>>(A, S, P);
+            k_level<false><<<grid, 256, 0, s>>>(A, S, P);
+            k_level_hub<false><<<hgrid, 256, 0, s>>>(A, S, P);
         }
         if (timeit) cudaEventRecord(ev1, s);
-        k_advance<CW><<<agrid, 256, 0, s>>>(A, S, F, P.N, Vis, P.X, xwords, P.nw, P.nchunk, A.nq, lists[cur ^ 1],
-                                            &P.ctrl->cnt[cur ^ 1]);
-        RPQ_CUDA_TRY(cudaMemcpyAsync(h_cnt, &P.ctrl->cnt[cur ^ 1], 4, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(&P.ctrl->cnt[cur], 0, 4, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(&P.ctrl->nhub_recs, 0, 4, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(h_flag, &P.ctrl->active[par ^ 1], 4, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(&P.ctrl->active[par], 0, 4, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(&P.ctrl->nhub_items, 0, 8, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
         RPQ_CUDA_TRY(cudaGetLastError());
         out_stats->expand_launches += 2;
-        out_stats->kernel_launches += 3;
+        out_stats->kernel_launches += 2;
         if (timeit) {
             float ms = 0;
             cudaEventElapsedTime(&ms, ev0, ev1);
             out_stats->expand_ms += ms;
         }
         ++levels;
-        n = *h_cnt;
-        cur ^= 1;
+        par ^= 1;
+        if (*h_flag == 0) break;
     }
     out_stats->levels += levels;
     return RPQ_OK;
@@ -723,9 +757,8 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     uint64_t budget = o.hbm_budget_bytes ? o.hbm_budget_bytes : (uint64_t)(free_b * 0.9);
     uint64_t B = o.batch_sources;
     if (B == 0) {
-        // bytes per 64-source word column: 24 R (Vis, F, N) + lists/bitmaps
-        // (2 x 8 B per chunk of >= 1 word, worst case CW = 1) + extraction
-        const double per_word = 24.0 * R_max + 17.0 * R_max + 64.0 * 8 * 2;
+        // bytes per 64-source word column
+        const double per_word = 16.0 * R_max + 0.5 * R_max + 64.0 * 8 * 2;   // Vis + N, bitmaps, extraction
         uint64_t nw_max = per_word > 0 ? (uint64_t)(budget / per_word) : 1;
         if (nw_max < 1) nw_max = 1;
         B = std::min<uint64_t>(std::max<uint64_t>(np, 1), nw_max * 64);
@@ -754,12 +787,12 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     // ---- workspace ----------------------------------------------------------
     const uint64_t words = R_max * nw;
     ST.state_words = words;
-    const uint64_t list_cap = std::max<uint64_t>(R_max * nchunk, B);
-    const uint64_t xwords = (R_max * nchunk + 31) / 32 + 1;
-    const uint32_t hrec_cap = 1u << 22;
-    uint64_t *Vis = nullptr, *F = nullptr, *N = nullptr;
-    uint32_t *X = nullptr;
-    Item *L0 = nullptr, *L1 = nullptr;
+    const uint64_t nxw = (nchunk + 31) / 32;            // X words per row
+    const uint64_t nxwords = R_max * nxw;
+    const uint64_t xbwords = (nxwords + 1023) / 1024 + 1;
+    const uint32_t hitem_cap = 1u << 14, hrec_cap = 1u << 22;
+    uint64_t *Vis = nullptr, *N = nullptr, *hubF = nullptr;
+    uint32_t *X0 = nullptr, *X1 = nullptr, *XB0 = nullptr, *XB1 = nullptr;
     Ctrl *ctrl = (Ctrl *)ws.get(sizeof(Ctrl));
     unsigned long long *d_stats = (unsigned long long *)ws.get(NSTAT * 8 + 8);
     unsigned long long *d_total = d_stats + NSTAT;
@@ -767,21 +800,26 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     RPQ_CUDA_TRY(cudaMallocHost(&h_cnt, 16));
     struct HostGuard { uint32_t *p; ~HostGuard() { cudaFreeHost(p); } } hg{h_cnt};
     HubRec *hrecs = nullptr;
+    HubItem *hitems = nullptr;
     if (nbatches) {
         Vis = (uint64_t *)ws.get(words * 8);
-        F = (uint64_t *)ws.get(words * 8);
         N = (uint64_t *)ws.get(words * 8);
-        X = (uint32_t *)ws.get(xwords * 4);
-        L0 = (Item *)ws.get(list_cap * sizeof(Item));
-        L1 = (Item *)ws.get(list_cap * sizeof(Item));
+        X0 = (uint32_t *)ws.get(nxwords * 4 + 128);
+        X1 = (uint32_t *)ws.get(nxwords * 4 + 128);
+        XB0 = (uint32_t *)ws.get(xbwords * 4);
+        XB1 = (uint32_t *)ws.get(xbwords * 4);
+        hitems = (HubItem *)ws.get((uint64_t)hitem_cap * sizeof(HubItem));
+        hubF = (uint64_t *)ws.get((uint64_t)hitem_cap * KGRP * 32 * 8);
         hrecs = (HubRec *)ws.get((uint64_t)hrec_cap * sizeof(HubRec));
-        if (!Vis || !F || !N || !X || !L0 || !L1 || !hrecs)
+        if (!Vis || !N || !X0 || !X1 || !XB0 || !XB1 || !hitems || !hubF || !hrecs)
             return fail(rpq_fail(RPQ_ENOMEM, "out of device memory for B=%llu sources (%llu state words)",
                                  (unsigned long long)B, (unsigned long long)words));
         RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(F, 0, words * 8, s));
         RPQ_CUDA_TRY(cudaMemsetAsync(N, 0, words * 8, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(X, 0, xwords * 4, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(X0, 0, nxwords * 4 + 128, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(X1, 0, nxwords * 4 + 128, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(XB0, 0, xbwords * 4, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(XB1, 0, xbwords * 4, s));
     }
     if (!ctrl || !d_stats) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory"));
     RPQ_CUDA_TRY(cudaMemsetAsync(d_stats, 0, NSTAT * 8 + 8, s));
@@ -852,27 +890,20 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         if (b != (uint64_t)o.shard_index) {   // visited words of the previous batch
             RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
         }
-        ExpandArgs P{};
-        P.F = F; P.N = N; P.Vis = Vis; P.X = X;
-        P.cur = L0; P.ctrl = ctrl; P.cur_idx = 0;
-        P.hrecs = hrecs; P.hrec_cap = hrec_cap;
-        P.nw = (uint32_t)nw; P.nchunk = (uint32_t)nchunk;
+        LevelArgs P{};
+        P.N = N; P.Vis = Vis;
+        P.nxwords = rows * nxw;
+        P.ctrl = ctrl; P.par = 0;
+        P.hitems = hitems; P.hubF = hubF; P.hrecs = hrecs;
+        P.hitem_cap = hitem_cap; P.hrec_cap = hrec_cap;
+        P.nw = (uint32_t)nw; P.nxw = (uint32_t)nxw; P.cw = CW;
         P.stats = d_stats;
-        rpq_status st = RPQ_OK;
-        switch (CW) {
-#define RPQ_CASE(C)                                                                                        \
-    case C:                                                                                                \
-        k_seed<C><<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, F, Vis, L0, ctrl, (uint32_t)nw);      \
-        ST.kernel_launches++;                                                                              \
-        st = run_levels<C>(A, S, P, F, Vis, L0, L1, xwords, s, stats, timeit, nb, h_cnt, &ST, evt0, evt1); \
-        break;
-            RPQ_CASE(1) RPQ_CASE(2) RPQ_CASE(4) RPQ_CASE(8) RPQ_CASE(16) RPQ_CASE(32)
-#undef RPQ_CASE
-        }
+        k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, N, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl);
+        ST.kernel_launches++;
+        rpq_status st = run_levels(A, S, P, X0, X1, XB0, XB1, s, stats, timeit, h_cnt, &ST, evt0, evt1);
         if (st != RPQ_OK) return fail(st);
-        // N and X are all zero again here (the last level activated nothing);
-        // F holds stale words that are never read without being rewritten.
-        // Extraction reads Vis of the final states.
+        // N, X and XB are all zero again here (the last level activated
+        // nothing).  Extraction reads Vis of the final states.
         const uint32_t vlo = fin_hull.empty() ? 0 : fin_hull.lo;
         const uint64_t vn = fin_hull.empty() ? 0 : (uint64_t)fin_hull.hi - fin_hull.lo + 1;
         const uint64_t eps_np = eps ? (jhi - jlo) - nb : 0;   // non-productive candidates in the interval
