@@ -1,0 +1,375 @@
+"""bench.py -- all-pairs RPQ throughput (product edges traversed per second).
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE
+JSON line on rank 0.  N>1 runs under torch.distributed.run, one process per
+GPU (NCCL): the source batches are sharded round-robin over ranks (batch b ->
+rank b % N), the graph is replicated, and only counts/PE are reduced.
+
+A step = one pass of the whole hot path over the workload: for each query of
+the workload, compile the regex and evaluate the all-pairs RPQ in COUNT mode
+(the paper's benchmark output) on the device-resident graph.
+Metric = PE / s where PE (product edges traversed, reading
+R12 in DESIGN.md) = sum over reached (vertex, state) pairs of the product
+out-degree on the minimal trim DFA -- identical for the GPU path and the
+oracle (pinned by tests).
+
+`--impl reference` times the CPU oracle (oracle/, O1) on a bounded seeded
+sample of the same workload, on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+WORKLOADS = {
+    # BASELINE.json configs[1]: random labelled graph, 100K vertices / 1M
+    # edges, 4 labels, RPQs a*, (a|b)*c, a b* c, all-pairs, 1 GPU
+    "cfg2": {"queries": ["a*", "(a|b)*c", "a b* c"],
+             "desc": "uniform random labelled graph |V|=100000 |E|=1000000 (distinct), 4 labels, seed 2"},
+}
+
+
+def make_graph(name):
+    import synth
+    if name == "cfg2":
+        return synth.uniform_graph(100_000, 1_000_000, 4, seed=2)
+    raise ValueError(name)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """ncu dram bytes per k_level launch for the default workload, committed
+    under profiles/ (see profiles/README.md); None if absent."""
+    p = os.path.join(ROOT, "profiles", "traffic_cfg2.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def algorithmic_bytes(st):
+    """Bytes the fused level kernel must move:
+    32 B per advanced word (N exch read+write, Vis read+write), 8 B per
+    (row-group, transition) offset pair, 4 B per (row-group, edge) neighbour
+    id, 16 B per (word, edge) operation (visited read + next-frontier OR)."""
+    return (32 * st["word_items"] + 8 * st["item_transitions"] + 4 * st["item_edges"]
+            + 16 * st["word_edge_ops"])
+
+
+# --------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2602_20748_b200 as R
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    wl = WORKLOADS[args.workload]
+    g = make_graph(args.workload)
+    G = R.rpq_graph_load(g, device=local, stream=sp)
+    queries = wl["queries"]
+
+    # batch width: one batch per rank for N > 1 (round-robin sharding)
+    probe = {}
+    for rx in queries:
+        a = R.rpq_compile(G, rx)
+        r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=sp, batch_sources=args.batch)
+        probe[rx] = r.stats()
+    bsz = {}
+    for rx in queries:
+        P = probe[rx]["productive_sources"]
+        if args.batch:
+            bsz[rx] = args.batch
+        elif world > 1:
+            bsz[rx] = int(-(-P // world) + 63) // 64 * 64
+        else:
+            bsz[rx] = 0
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")   # > 126 MB L2
+
+    def step(mode):
+        tot = {"count": 0, "pe": 0, "launches": 0, "expand_ms": 0.0, "bytes": 0, "expand_launches": 0}
+        for rx in queries:
+            a = R.rpq_compile(G, rx)
+            r = R.rpq_eval_allpairs(G, a, mode=mode, stream=sp, batch_sources=bsz[rx],
+                                    shard_index=rank, shard_count=world)
+            st = r.stats()
+            tot["count"] += r.count
+            tot["pe"] += st["product_edges"]
+            tot["launches"] += st["kernel_launches"]
+            tot["expand_ms"] += st["expand_ms"]
+            tot["expand_launches"] += st["expand_launches"]
+            tot["bytes"] += algorithmic_bytes(st)
+        return tot
+
+    mode = R.RPQ_COUNT | R.RPQ_STATS | R.RPQ_TIME_KERNELS
+    for _ in range(args.warmup):
+        step(mode)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    times, agg = [], None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)                       # evict L2 between timed steps (untimed)
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            t = step(mode)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+            if agg is None:
+                agg = dict(t)
+            else:
+                for k in agg:
+                    agg[k] += t[k]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = float(sum(times))
+    pe_total = agg["pe"]
+    if world > 1:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        pt = torch.tensor([float(pe_total), float(agg["count"])], dtype=torch.float64, device="cuda")
+        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
+        pe_total, count_total = int(pt[0].item()), int(pt[1].item())
+    else:
+        count_total = agg["count"]
+
+    # end to end through the public API: host (pinned) edge arrays -> load ->
+    # compile -> evaluate -> counts on the host, every step
+    e2e_ms = []
+    pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in
+           {"src": g.src, "dst": g.dst, "lab": g.label.astype(np.int16)}.items()}
+    h_src, h_dst = pin["src"].numpy(), pin["dst"].numpy()
+    h_lab = pin["lab"].numpy().view(np.uint16)
+    h2d = int(h_src.nbytes + h_dst.nbytes + h_lab.nbytes)
+    e2e_steps = max(1, min(args.steps, 5))
+    for i in range(e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        G2 = R.rpq_graph_load(num_vertices=g.num_vertices, src=h_src, dst=h_dst, label=h_lab,
+                              label_names=g.label_names, device=local, stream=sp)
+        pe_e = 0
+        for rx in queries:
+            a = R.rpq_compile(G2, rx)
+            r = R.rpq_eval_allpairs(G2, a, mode=R.RPQ_COUNT, stream=sp, batch_sources=bsz[rx],
+                                    shard_index=rank, shard_count=world)
+            _ = r.count                                  # device -> host result
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) * 1e3
+        del G2
+        if i > 0:
+            e2e_ms.append(dt)
+    e2e_step = statistics.median(e2e_ms)
+    if world > 1:
+        tt = torch.tensor([e2e_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_step = float(tt.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    pe_per_step = pe_total / args.steps
+    value = pe_total / (total_ms / 1e3)
+    peak, peak_src = load_peaks()
+    achieved = agg["bytes"] / (agg["expand_ms"] / 1e3) / 1e9 if agg["expand_ms"] > 0 else None
+    per_launch = agg["bytes"] / max(1, agg["expand_launches"])
+    traffic = load_traffic()
+    line = {
+        "metric": "all-pairs RPQ product-edges traversed/s",
+        "value": value,
+        "unit": "PE/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "u64",
+        "data": "synthetic",
+        "config": {"workload": args.workload, "graph": wl["desc"], "queries": queries, "mode": "COUNT",
+                   "pe_per_step": pe_per_step, "pairs_per_step": count_total / args.steps,
+                   "batch_sources": {rx: probe[rx]["batch_sources"] if not bsz[rx] else bsz[rx] for rx in queries},
+                   "parallelism": f"source-batch shards x{world}",
+                   "l2": "flushed between timed steps (256 MiB write)"},
+        "roofline": {"bound": "hbm", "kernel": "k_level (+k_level_hub)", "achieved": achieved, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "algorithmic_bytes_per_launch": per_launch,
+                     "launches": agg["expand_launches"],
+                     "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                     "traffic_source": traffic.get("source") if traffic else None},
+        "e2e": {"value": pe_per_step / (e2e_step / 1e3), "unit": "PE/s", "ms_per_step": e2e_step,
+                "h2d_bytes_per_step": h2d * 1, "d2h_bytes_per_step": 8 * len(queries),
+                "includes": "rpq_graph_load from pinned host arrays + compile + eval + count readback"},
+        "gpu_launches": agg["launches"],
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, g, queries, budget_s=args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------
+def oracle_sample(g, queries, budget_s, seed=0):
+    """Time the oracle (O1, all host threads) on seeded source samples of the
+    workload, growing the sample until ~budget_s seconds of CPU work."""
+    import oracle
+    og = oracle.OracleGraph(g)
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(seed)
+    order = rng.permutation(g.num_vertices).astype(np.uint32)
+    n, pe, secs, used = 64, 0, 0.0, 0
+    while secs < budget_s and used < g.num_vertices:
+        srcs = np.sort(order[used:used + n])
+        t0 = time.perf_counter()
+        for rx in queries:
+            r = oracle.eval_sources(og, rx, srcs, pairs=False, threads=threads)
+            pe += int(r["pe"].sum())
+        secs += time.perf_counter() - t0
+        used += srcs.size
+        n = min(n * 2, 1 << 16)
+    return pe, secs, used, threads
+
+
+def cpu_baseline(args, g, queries, budget_s):
+    pe, secs, used, threads = oracle_sample(g, queries, budget_s)
+    return {"value": pe / secs, "unit": "PE/s", "cores": threads, "kind": "oracle",
+            "sample": f"{used} seeded random sources x {len(queries)} queries of {args.workload} "
+                      f"({pe:.3e} PE in {secs:.1f} s)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    wl = WORKLOADS[args.workload]
+    g = make_graph(args.workload)
+    queries = wl["queries"]
+    per_step = args.ref_step_seconds
+    for _ in range(args.warmup):
+        oracle_sample(g, queries, per_step / 4, seed=1)
+    pe_tot, s_tot, used_tot, threads = 0, 0.0, 0, 1
+    for k in range(args.steps):
+        pe, secs, used, threads = oracle_sample(g, queries, per_step, seed=100 + k)
+        pe_tot += pe
+        s_tot += secs
+        used_tot += used
+    value = pe_tot / s_tot
+    line = {"impl": "reference", "metric": "all-pairs RPQ product-edges traversed/s", "value": value,
+            "unit": "PE/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": s_tot * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": args.workload, "graph": wl["desc"], "queries": queries, "mode": "COUNT"},
+            "cpu_baseline": {"value": value, "unit": "PE/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{used_tot} seeded random sources x {len(queries)} queries over "
+                                       f"{args.steps} steps"},
+            "e2e": {"value": value, "unit": "PE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
+    ap.add_argument("--batch", type=int, default=0, help="source batch width B (0 = auto)")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -17,7 +17,9 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librpq.so")
+# RPQ_LIB_PATH selects an alternative build of the same library (kernel
+# tuning experiments); the default is the in-tree librpq.so
+LIB_PATH = os.environ.get("RPQ_LIB_PATH") or os.path.join(_HERE, "librpq.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build()); "

@@ -34,6 +34,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
@@ -52,8 +54,12 @@ constexpr uint32_t HUB_EDGES = 512;      // edges per hub segment
 constexpr int TILE_V = 1024;             // vertices per extraction tile
 constexpr int NSTAT = 8;
 #ifndef RPQ_LEVEL_MINB
-#define RPQ_LEVEL_MINB 2
+#define RPQ_LEVEL_MINB 3
 #endif
+#ifndef RPQ_SLOTS
+#define RPQ_SLOTS 8
+#endif
+constexpr int SLOTS = RPQ_SLOTS;          // visited-word loads in flight per lane
 constexpr int KGRP = 8;                 // chunks of a row advanced/expanded together
 
 struct DevAuto {
@@ -144,18 +150,21 @@ template <int KC, bool STATS>
 __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S, uint32_t q2,
                                              const uint32_t *__restrict__ nbr, uint32_t beg, uint32_t end,
                                              const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
-                                             unsigned long long *st) {
-    constexpr int E = KGRP / KC;
+                                             unsigned long long *st, bool &act) {
+    constexpr int E = SLOTS / KC;
     const uint32_t tbase = (uint32_t)(S.row_base[q2] - S.lo[q2]);
     const uint32_t colbase = xw * 32u * p.cw + lane;
     int fpop = 0, nzw = 0;
 #pragma unroll
     for (int k = 0; k < KC; ++k) { fpop += __popcll(f[k]); nzw += f[k] != 0; }
+    uint32_t ckk[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) ckk[k] = ((uint32_t)(bits >> (8 * k)) & 0xffu) * p.cw;
     for (uint32_t j = beg; j < end; j += 32) {
         const uint32_t my = (j + lane < end) ? __ldg(nbr + j + lane) : 0u;
         const int cnt = (int)((end - j) < 32u ? (end - j) : 32u);
         for (int e0 = 0; e0 < cnt; e0 += E) {
-            uint32_t trow[E], xo[E];
+            uint32_t trow[E];
             uint64_t vis[E][KC];
 #pragma unroll
             for (int e = 0; e < E; ++e) {
@@ -163,11 +172,7 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
                 trow[e] = tbase + __shfl_sync(0xffffffffu, my, (e0 + e) & 31);
                 const uint64_t rb = (uint64_t)trow[e] * p.nw + colbase;
 #pragma unroll
-                for (int k = 0; k < KC; ++k) {
-                    const uint32_t ck = (uint32_t)(bits >> (8 * k)) & 0xffu;
-                    vis[e][k] = (ok && f[k]) ? ld_cg(p.Vis + rb + ck * p.cw) : ~0ull;
-                }
-                xo[e] = (lane == 0 && ok) ? __ldcg(p.Xnext + (uint64_t)trow[e] * p.nxw + xw) : ~0u;
+                for (int k = 0; k < KC; ++k) vis[e][k] = (ok && f[k]) ? ld_cg(p.Vis + rb + ckk[k]) : ~0ull;
             }
 #pragma unroll
             for (int e = 0; e < E; ++e) {
@@ -175,19 +180,20 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
                 const uint64_t rb = (uint64_t)trow[e] * p.nw + colbase;
 #pragma unroll
                 for (int k = 0; k < KC; ++k) {
-                    const uint32_t ck = (uint32_t)(bits >> (8 * k)) & 0xffu;
                     const uint64_t m = f[k] & ~vis[e][k];
                     if (m) {
-                        red_or64(p.N + rb + ck * p.cw, m);
+                        red_or64(p.N + rb + ckk[k], m);
                         if (STATS) st[S_N_RED]++;
                     }
-                    if (__ballot_sync(0xffffffffu, m != 0)) newmask |= 1u << ck;
+                    if (__ballot_sync(0xffffffffu, m != 0)) newmask |= 1u << ((bits >> (8 * k)) & 0xffu);
                 }
-                if (lane == 0 && (newmask & ~xo[e])) {
+                if (lane == 0 && newmask) {
+                    // activity of the target row: fire-and-forget ORs (the
+                    // words are idempotent; no test load on the critical path)
                     const uint64_t xi = (uint64_t)trow[e] * p.nxw + xw;
                     red_or32(p.Xnext + xi, newmask);
                     red_or32(p.XBnext + (xi >> 10), 1u << ((xi >> 5) & 31));
-                    p.ctrl->active[p.par ^ 1] = 1u;
+                    act = true;
                     if (STATS) st[S_X_RED]++;
                 }
             }
@@ -217,11 +223,11 @@ template <bool STATS>
 __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const Layout &S, uint32_t q2,
                                                const uint32_t *nbr, uint32_t beg, uint32_t end,
                                                const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
-                                               unsigned long long *st) {
-    if (nk > 4) expand_edges<8, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st);
-    else if (nk > 2) expand_edges<4, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st);
-    else if (nk > 1) expand_edges<2, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st);
-    else expand_edges<1, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st);
+                                               unsigned long long *st, bool &act) {
+    if (nk > 4) expand_edges<8, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act);
+    else if (nk > 2) expand_edges<4, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act);
+    else if (nk > 1) expand_edges<2, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act);
+    else expand_edges<1, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act);
 }
 
 // Main level kernel: a warp owns one active X word = one row and up to 32 of
@@ -236,6 +242,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
     const uint64_t nunits = (p.nxwords + 31) >> 5;
     unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool act = false;
     for (uint64_t u = wid; u < nunits; u += nwarps) {
         const uint32_t xb = __ldcg(p.XBcur + (u >> 5));
         if (!((xb >> (u & 31)) & 1u)) continue;
@@ -324,11 +331,12 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                                 p.hrecs[r + sg] = HubRec{0u, 0u, 0u, 0u};
                         }
                     }
-                    dispatch_edges<STATS>(nk, p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st);
+                    dispatch_edges<STATS>(nk, p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act);
                 }
             }
         }
     }
+    if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
     flush_stats<STATS>(st, p.stats);
 }
 
@@ -340,6 +348,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
     const uint32_t n = min(p.ctrl->nhub_recs, p.hrec_cap);
     unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool act = false;
     for (uint64_t it = wid; it < n; it += nwarps) {
         const HubRec r = p.hrecs[it];
         if (r.end == r.beg) continue;
@@ -348,8 +357,9 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto
 #pragma unroll
         for (int k = 0; k < KGRP; ++k) f[k] = p.hubF[((uint64_t)r.hitem * KGRP + k) * 32 + lane];
         dispatch_edges<STATS>((int)h.nk, p, S, A.tto[r.t], A.nbr[A.tslot[r.t]], r.beg, r.end, f, h.bits, h.xw, lane,
-                              st);
+                              st, act);
     }
+    if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
     flush_stats<STATS>(st, p.stats);
 }
 
@@ -571,6 +581,23 @@ __global__ void k_write_eps(const uint8_t *flag, const uint32_t *cand, uint64_t 
     }
 }
 
+// RPQ_DEBUG_TIMING=1: print host-observed phase times (synchronising)
+struct PhaseTimer {
+    bool on;
+    cudaStream_t s;
+    std::chrono::steady_clock::time_point t;
+    explicit PhaseTimer(cudaStream_t st) : on(getenv("RPQ_DEBUG_TIMING") != nullptr), s(st) {
+        t = std::chrono::steady_clock::now();
+    }
+    void mark(const char *what) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[rpq] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
+
 struct NZ {
     __host__ __device__ bool operator()(const unsigned long long &x) const { return x != 0; }
 };
@@ -675,6 +702,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     cudaEvent_t evs[4] = {evt0, evt1, e_begin, e_end};
     EvGuard eg{evs};
     cudaEventRecord(e_begin, s);
+    PhaseTimer PT(s);
     rpq_stats &ST = res->stats;
 
     // ---- device automaton ------------------------------------------------
@@ -726,6 +754,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaMemsetAsync(flag, 0, nsrc, s));
     }
     ST.productive_sources = np;
+    PT.mark("productive sources");
     const bool eps = a->accepts_empty;
 
     // ---- ranges per state (hull of dst ranges of entering labels) ---------
@@ -784,6 +813,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     }
     RPQ_CUDA_TRY(cudaStreamSynchronize(s));
 
+    PT.mark("batch plan");
     // ---- workspace ----------------------------------------------------------
     const uint64_t words = R_max * nw;
     ST.state_words = words;
@@ -796,9 +826,9 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     Ctrl *ctrl = (Ctrl *)ws.get(sizeof(Ctrl));
     unsigned long long *d_stats = (unsigned long long *)ws.get(NSTAT * 8 + 8);
     unsigned long long *d_total = d_stats + NSTAT;
-    uint32_t *h_cnt = nullptr;
-    RPQ_CUDA_TRY(cudaMallocHost(&h_cnt, 16));
-    struct HostGuard { uint32_t *p; ~HostGuard() { cudaFreeHost(p); } } hg{h_cnt};
+    // small pinned host word for the per-level flag readback (per thread)
+    static thread_local uint32_t *h_cnt = nullptr;
+    if (!h_cnt) RPQ_CUDA_TRY(cudaMallocHost(&h_cnt, 64));
     HubRec *hrecs = nullptr;
     HubItem *hitems = nullptr;
     if (nbatches) {
@@ -824,6 +854,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     if (!ctrl || !d_stats) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory"));
     RPQ_CUDA_TRY(cudaMemsetAsync(d_stats, 0, NSTAT * 8 + 8, s));
 
+    PT.mark("workspace alloc + clear");
     // per-candidate counts (PER_SOURCE / PAIRS), initialised to the epsilon pair
     unsigned long long *cand_cnt = nullptr;
     if (want_ps) {
@@ -900,7 +931,9 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         P.stats = d_stats;
         k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, N, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl);
         ST.kernel_launches++;
+        PT.mark("seed");
         rpq_status st = run_levels(A, S, P, X0, X1, XB0, XB1, s, stats, timeit, h_cnt, &ST, evt0, evt1);
+        PT.mark("levels");
         if (st != RPQ_OK) return fail(st);
         // N, X and XB are all zero again here (the last level activated
         // nothing).  Extraction reads Vis of the final states.
@@ -968,6 +1001,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaGetLastError());
     }
 
+    PT.mark("extraction");
     // ---- result assembly ---------------------------------------------------
     res->count = total;
     if (want_pairs) {
@@ -1034,6 +1068,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     float tms = 0;
     cudaEventElapsedTime(&tms, e_begin, e_end);
     ST.total_ms = tms;
+    PT.mark("assembly");
     RPQ_CUDA_TRY(cudaGetLastError());
     *out = res;
     return RPQ_OK;

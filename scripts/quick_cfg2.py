@@ -7,7 +7,8 @@ g = synth.uniform_graph()
 torch.cuda.init()
 s = torch.cuda.current_stream().cuda_stream
 G = R.rpq_graph_load(g, stream=s)
-for B in [0, 8192, 2048]:
+Bs = [int(x) for x in sys.argv[1].split(',')] if len(sys.argv) > 1 else [0, 8192, 2048]
+for B in Bs:
     for rx in ["a*", "(a|b)*c", "a b* c"]:
         a = R.rpq_compile(G, rx)
         r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, batch_sources=B, stream=s)
