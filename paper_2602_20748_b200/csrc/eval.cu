@@ -95,6 +95,8 @@ struct Ctrl {                  // per-level device counters / flags
     uint32_t active[2];        // "some row was activated" flag per level parity
     uint32_t nhub_items;
     uint32_t nhub_recs;
+    uint32_t levels;           // levels run (device-side loop)
+    uint32_t pad[3];
 };
 
 // One BFS level over the rows whose activity bit is set in (Xcur, XBcur).
@@ -133,6 +135,35 @@ __device__ __forceinline__ void red_or32(uint32_t *p, uint32_t v) {
 }
 __device__ __forceinline__ void red_and32(uint32_t *p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// the per-batch layout lives in device memory (so a captured level graph is
+// reusable across batches); each CTA stages it in shared memory
+__device__ __forceinline__ void load_layout(Layout &S, const Layout *__restrict__ Sg, uint32_t nq) {
+    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
+        S.row_base[q] = Sg->row_base[q];
+        S.lo[q] = Sg->lo[q];
+        S.len[q] = Sg->len[q];
+    }
+    __syncthreads();
+}
+
+// Between the two levels of the graph body / at its end: reset the counters
+// the next level needs, count levels, and (end) decide whether to loop.
+__global__ void k_level_mid(Ctrl *ctrl, int par) {
+    ctrl->active[par] = 0;        // the next level (parity par ^ 1) sets active[par]
+    ctrl->nhub_items = 0;
+    ctrl->nhub_recs = 0;
+    ctrl->levels += 1;
+}
+
+__global__ void k_level_end(Ctrl *ctrl, int par, cudaGraphConditionalHandle h) {
+    const uint32_t go = ctrl->active[par ^ 1];
+    ctrl->active[par] = 0;
+    ctrl->nhub_items = 0;
+    ctrl->nhub_recs = 0;
+    ctrl->levels += 1;
+    cudaGraphSetConditional(h, go ? 1u : 0u);
 }
 
 __device__ __forceinline__ int row_state(const Layout &S, uint32_t nq, uint64_t row) {
@@ -236,7 +267,10 @@ __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const
 // transition of the row's state.  Work units (32 X words = one XB bit) are
 // interleaved over warps.
 template <bool STATS>
-__global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, const Layout S, const LevelArgs p) {
+__global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, const Layout *__restrict__ Sg,
+                                                               const LevelArgs p) {
+    __shared__ Layout S;
+    load_layout(S, Sg, A.nq);
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -342,7 +376,10 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
 
 // Deferred long rows: a warp per HUB_EDGES-edge segment.
 template <bool STATS>
-__global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto A, const Layout S, const LevelArgs p) {
+__global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto A, const Layout *__restrict__ Sg,
+                                                                   const LevelArgs p) {
+    __shared__ Layout S;
+    load_layout(S, Sg, A.nq);
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -628,47 +665,88 @@ Range hull(Range a, Range b) {
     return {std::min(a.lo, b.lo), std::max(a.hi, b.hi)};
 }
 
-rpq_status run_levels(const DevAuto &A, const Layout &S, LevelArgs P, uint32_t *X0, uint32_t *X1, uint32_t *XB0,
-                      uint32_t *XB1, cudaStream_t s, bool stats, bool timeit, uint32_t *h_flag, rpq_stats *out_stats,
-                      cudaEvent_t ev0, cudaEvent_t ev1) {
-    // one level = k_level (+ hub segments); the host only reads a 4-byte
-    // "anything activated" flag per level
-    const uint64_t nunits = (P.nxwords + 31) / 32;
-    const int grid = grid_for(nunits * 32, 256, 148 * 3);
-    const int hgrid = 148 * 3;
+// Level loop, device-driven: a CUDA graph whose body is a conditional WHILE
+// node running two levels (parity 0, then 1) per iteration; the end kernel
+// sets the loop condition from the "activated" flag, so a whole batch runs
+// without a host round trip per level.  (An empty extra level costs one
+// scan of the tiny XB bitmap.)
+struct LevelGraph {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~LevelGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (g) cudaGraphDestroy(g);
+    }
+};
+
+template <bool STATS>
+cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg, const LevelArgs &P0,
+                              const LevelArgs &P1, int grid, int hgrid) {
+    cudaError_t e;
+    if ((e = cudaGraphCreate(&LG.g, 0)) != cudaSuccess) return e;
+    cudaGraphConditionalHandle h;
+    if ((e = cudaGraphConditionalHandleCreate(&h, LG.g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) return e;
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    if ((e = cudaGraphAddNode(&cn, LG.g, nullptr, 0, &cp)) != cudaSuccess) return e;
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraphNode_t prev = nullptr;
+    auto add = [&](void *fn, dim3 gr, dim3 bl, void **args) -> cudaError_t {
+        cudaKernelNodeParams kp{};
+        kp.func = fn;
+        kp.gridDim = gr;
+        kp.blockDim = bl;
+        kp.sharedMemBytes = 0;
+        kp.kernelParams = args;
+        cudaGraphNode_t n;
+        cudaError_t r = cudaGraphAddKernelNode(&n, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp);
+        prev = n;
+        return r;
+    };
+    DevAuto a = A;
+    const Layout *sg = Sg;
+    LevelArgs p0 = P0, p1 = P1;
+    Ctrl *ctrl = P0.ctrl;
+    int par0 = 0, par1 = 1;
+    void *a0[] = {&a, &sg, &p0};
+    void *a1[] = {&a, &sg, &p1};
+    void *m0[] = {&ctrl, &par0};
+    void *m1[] = {&ctrl, &par1, &h};
+    if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a0)) != cudaSuccess) return e;
+    if ((e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
+    if ((e = add((void *)k_level_mid, dim3(1), dim3(1), m0)) != cudaSuccess) return e;
+    if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a1)) != cudaSuccess) return e;
+    if ((e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
+    if ((e = add((void *)k_level_end, dim3(1), dim3(1), m1)) != cudaSuccess) return e;
+    return cudaGraphInstantiate(&LG.exec, LG.g, 0);
+}
+
+// Level loop, host-driven (RPQ_HOST_LOOP=1, or if graph creation fails):
+// one flag readback per level.
+rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &P0, const LevelArgs &P1, int grid,
+                           int hgrid, cudaStream_t s, bool stats, uint32_t *h_flag, rpq_stats *out_stats) {
     int par = 0;
-    uint32_t levels = 0;
-    uint32_t *X[2] = {X0, X1}, *XB[2] = {XB0, XB1};
     for (;;) {
-        P.par = par;
-        P.Xcur = X[par]; P.Xnext = X[par ^ 1];
-        P.XBcur = XB[par]; P.XBnext = XB[par ^ 1];
-        if (timeit) cudaEventRecord(ev0, s);
+        const LevelArgs &P = par ? P1 : P0;
         if (stats) {
-            k_level<true><<<grid, 256, 0, s>>>(A, S, P);
-            k_level_hub<true><<<hgrid, 256, 0, s>>>(A, S, P);
+            k_level<true><<<grid, 256, 0, s>>>(A, Sg, P);
+            k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
         } else {
-            k_level<false><<<grid, 256, 0, s>>>(A, S, P);
-            k_level_hub<false><<<hgrid, 256, 0, s>>>(A, S, P);
+            k_level<false><<<grid, 256, 0, s>>>(A, Sg, P);
+            k_level_hub<false><<<hgrid, 256, 0, s>>>(A, Sg, P);
         }
-        if (timeit) cudaEventRecord(ev1, s);
         RPQ_CUDA_TRY(cudaMemcpyAsync(h_flag, &P.ctrl->active[par ^ 1], 4, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(&P.ctrl->active[par], 0, 4, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(&P.ctrl->nhub_items, 0, 8, s));
+        k_level_mid<<<1, 1, 0, s>>>(P.ctrl, par);
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
         RPQ_CUDA_TRY(cudaGetLastError());
-        out_stats->expand_launches += 2;
-        out_stats->kernel_launches += 2;
-        if (timeit) {
-            float ms = 0;
-            cudaEventElapsedTime(&ms, ev0, ev1);
-            out_stats->expand_ms += ms;
-        }
-        ++levels;
+        out_stats->kernel_launches += 3;
         par ^= 1;
         if (*h_flag == 0) break;
     }
-    out_stats->levels += levels;
     return RPQ_OK;
 }
 
@@ -853,6 +931,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     }
     if (!ctrl || !d_stats) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory"));
     RPQ_CUDA_TRY(cudaMemsetAsync(d_stats, 0, NSTAT * 8 + 8, s));
+    RPQ_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s));
 
     PT.mark("workspace alloc + clear");
     // per-candidate counts (PER_SOURCE / PAIRS), initialised to the epsilon pair
@@ -872,6 +951,36 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     // it contribute their epsilon pair); one virtual batch when P is empty
     auto jstart = [&](uint64_t b) -> uint64_t { return b == 0 ? 0 : (b < nbatches ? bfirst[b] : nsrc); };
     const uint64_t nb_eff = std::max<uint64_t>(nbatches, 1);
+
+    // ---- level loop setup: parity-0/1 argument sets and the device graph ----
+    Layout *d_layout = (Layout *)ws.get(sizeof(Layout));
+    if (!d_layout) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+    LevelArgs P0{}, P1{};
+    P0.N = N; P0.Vis = Vis;
+    P0.Xcur = X0; P0.Xnext = X1; P0.XBcur = XB0; P0.XBnext = XB1;
+    P0.nxwords = nxwords;
+    P0.ctrl = ctrl; P0.par = 0;
+    P0.hitems = hitems; P0.hubF = hubF; P0.hrecs = hrecs;
+    P0.hitem_cap = hitem_cap; P0.hrec_cap = hrec_cap;
+    P0.nw = (uint32_t)nw; P0.nxw = (uint32_t)nxw; P0.cw = CW;
+    P0.stats = d_stats;
+    P1 = P0;
+    P1.par = 1;
+    std::swap(P1.Xcur, P1.Xnext);
+    std::swap(P1.XBcur, P1.XBnext);
+    const int lgrid = grid_for(((nxwords + 31) / 32) * 32, 256, 148 * RPQ_LEVEL_MINB);
+    const int hgrid = 148 * RPQ_LEVEL_MINB;
+    LevelGraph LG;
+    if (nbatches && !getenv("RPQ_HOST_LOOP")) {
+        cudaError_t ge = stats ? build_level_graph<true>(LG, A, d_layout, P0, P1, lgrid, hgrid)
+                               : build_level_graph<false>(LG, A, d_layout, P0, P1, lgrid, hgrid);
+        if (ge != cudaSuccess) {   // fall back to the host-driven loop
+            cudaGetLastError();
+            if (LG.exec) cudaGraphExecDestroy(LG.exec);
+            LG.exec = nullptr;
+        }
+    }
+    PT.mark("level graph");
 
     for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count) {
         const uint64_t jlo = jstart(b), jhi = (b + 1 < nb_eff) ? jstart(b + 1) : nsrc;
@@ -921,18 +1030,25 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         if (b != (uint64_t)o.shard_index) {   // visited words of the previous batch
             RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
         }
-        LevelArgs P{};
-        P.N = N; P.Vis = Vis;
-        P.nxwords = rows * nxw;
-        P.ctrl = ctrl; P.par = 0;
-        P.hitems = hitems; P.hubF = hubF; P.hrecs = hrecs;
-        P.hitem_cap = hitem_cap; P.hrec_cap = hrec_cap;
-        P.nw = (uint32_t)nw; P.nxw = (uint32_t)nxw; P.cw = CW;
-        P.stats = d_stats;
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, &S, sizeof(Layout), cudaMemcpyHostToDevice, s));
         k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, N, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl);
         ST.kernel_launches++;
         PT.mark("seed");
-        rpq_status st = run_levels(A, S, P, X0, X1, XB0, XB1, s, stats, timeit, h_cnt, &ST, evt0, evt1);
+        rpq_status st = RPQ_OK;
+        if (timeit) cudaEventRecord(evt0, s);
+        if (LG.exec) {
+            cudaError_t ge = cudaGraphLaunch(LG.exec, s);
+            if (ge != cudaSuccess) st = rpq_fail(RPQ_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(ge));
+        } else {
+            st = run_levels_host(A, d_layout, P0, P1, lgrid, hgrid, s, stats, h_cnt, &ST);
+        }
+        if (timeit) {
+            cudaEventRecord(evt1, s);
+            cudaEventSynchronize(evt1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, evt0, evt1);
+            ST.expand_ms += ms;
+        }
         PT.mark("levels");
         if (st != RPQ_OK) return fail(st);
         // N, X and XB are all zero again here (the last level activated
@@ -1049,6 +1165,14 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         cub::DeviceSelect::If(tmp, tb1, cand_cnt, (unsigned long long *)res->ps_cnt, d_n, (int64_t)nsrc, NZ(), s);
         cub::DeviceSelect::FlaggedIf(tmp, tb2, cand, cand_cnt, res->ps_src, d_n, (int64_t)nsrc, NZ(), s);
         RPQ_CUDA_TRY(cudaMemcpyAsync(&res->n_ps, d_n, 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (nbatches) {
+        Ctrl hc{};
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        ST.levels = hc.levels;
+        if (LG.exec) ST.kernel_launches += 3ull * hc.levels;
+        ST.expand_launches = 2ull * ST.levels;
     }
     if (stats) {
         unsigned long long hs[NSTAT];
