@@ -96,6 +96,8 @@ struct Ctrl {                  // per-level device counters / flags
     uint32_t nhub_items;
     uint32_t nhub_recs;
     uint32_t levels;           // levels run (device-side loop)
+    uint32_t ucnt[2];          // active work units listed for the level of each parity
+    uint32_t ucur[2];          // work-unit cursor (dynamic fetch) per parity
     uint32_t pad[3];
 };
 
@@ -118,6 +120,7 @@ struct LevelArgs {
     uint32_t nw;               // words per row
     uint32_t nxw;              // X words per row
     uint32_t cw;               // words per chunk (power of two <= 32)
+    uint32_t *ulist;           // active work units of the level (k_units)
     unsigned long long *stats;
 };
 
@@ -133,9 +136,6 @@ __device__ __forceinline__ void red_or64(uint64_t *p, uint64_t v) {
 __device__ __forceinline__ void red_or32(uint32_t *p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__device__ __forceinline__ void red_and32(uint32_t *p, uint32_t v) {
-    asm volatile("red.relaxed.gpu.global.and.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // the per-batch layout lives in device memory (so a captured level graph is
 // reusable across batches); each CTA stages it in shared memory
@@ -148,22 +148,47 @@ __device__ __forceinline__ void load_layout(Layout &S, const Layout *__restrict_
     __syncthreads();
 }
 
-// Between the two levels of the graph body / at its end: reset the counters
-// the next level needs, count levels, and (end) decide whether to loop.
-__global__ void k_level_mid(Ctrl *ctrl, int par) {
-    ctrl->active[par] = 0;        // the next level (parity par ^ 1) sets active[par]
-    ctrl->nhub_items = 0;
-    ctrl->nhub_recs = 0;
-    ctrl->levels += 1;
+// Before every level: list the active work units (set bits of XBcur, one
+// unit = 32 X words) for dynamic fetching, clear XBcur, and reset the
+// counters of the other parity / the hub buffers.  Block 0 does the resets.
+__global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
+    const int par = p.par;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        p.ctrl->ucnt[par ^ 1] = 0;
+        p.ctrl->ucur[par ^ 1] = 0;
+        p.ctrl->active[par ^ 1] = 0;   // set by this level's activations
+        p.ctrl->nhub_items = 0;
+        p.ctrl->nhub_recs = 0;
+        p.ctrl->levels += 1;
+    }
+    const int lane = threadIdx.x & 31;
+    for (uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; w0 < nxbwords;
+         w0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = w0 + lane;
+        uint32_t x = w < nxbwords ? __ldcg(p.XBcur + w) : 0u;
+        if (x) p.XBcur[w] = 0u;
+        const int c = __popc(x);
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        if (!tot) continue;
+        uint32_t base = 0;
+        if (lane == 31) base = atomicAdd(&p.ctrl->ucnt[par], (uint32_t)tot);
+        base = __shfl_sync(0xffffffffu, base, 31) + (uint32_t)(incl - c);
+        while (x) {
+            const int b = __ffs(x) - 1;
+            x &= x - 1;
+            p.ulist[base++] = (uint32_t)(w * 32 + b);
+        }
+    }
 }
 
-__global__ void k_level_end(Ctrl *ctrl, int par, cudaGraphConditionalHandle h) {
-    const uint32_t go = ctrl->active[par ^ 1];
-    ctrl->active[par] = 0;
-    ctrl->nhub_items = 0;
-    ctrl->nhub_recs = 0;
-    ctrl->levels += 1;
-    cudaGraphSetConditional(h, go ? 1u : 0u);
+__global__ void k_level_end(Ctrl *ctrl, cudaGraphConditionalHandle h) {
+    cudaGraphSetConditional(h, ctrl->active[0] ? 1u : 0u);   // activations of the parity-1 level
 }
 
 __device__ __forceinline__ int row_state(const Layout &S, uint32_t nq, uint64_t row) {
@@ -274,13 +299,16 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    const uint64_t nunits = (p.nxwords + 31) >> 5;
+    const uint32_t nunits = *(volatile uint32_t *)&p.ctrl->ucnt[p.par];
     unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool act = false;
-    for (uint64_t u = wid; u < nunits; u += nwarps) {
-        const uint32_t xb = __ldcg(p.XBcur + (u >> 5));
-        if (!((xb >> (u & 31)) & 1u)) continue;
-        if (lane == 0) red_and32(p.XBcur + (u >> 5), ~(1u << (u & 31)));
+    (void)wid; (void)nwarps;
+    for (;;) {
+        uint32_t ui = 0;
+        if (lane == 0) ui = atomicAdd(&p.ctrl->ucur[p.par], 1u);
+        ui = __shfl_sync(0xffffffffu, ui, 0);
+        if (ui >= nunits) break;
+        const uint64_t u = p.ulist[ui];
         const uint64_t xi_l = u * 32 + lane;
         const uint32_t xl = xi_l < p.nxwords ? __ldcg(p.Xcur + xi_l) : 0u;
         if (xl) p.Xcur[xi_l] = 0u;
@@ -296,9 +324,19 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
             const uint32_t v = S.lo[q] + (uint32_t)(row - S.row_base[q]);
             const uint64_t rb = row * p.nw + xw * 32u * p.cw + lane;
             const bool lane_ok = lane < (int)p.cw;
+            // prefetch the CSR row bounds of every transition of q (lane t
+            // holds transition toff[q] + t) while the advance runs
+            const int t0 = A.toff[q], ntr = A.toff[q + 1] - t0;
+            uint32_t obeg = 0, oend = 0;
+            if (lane < ntr) {
+                const uint32_t *off = A.off[A.tslot[t0 + lane]];
+                obeg = __ldg(off + v);
+                oend = __ldg(off + v + 1);
+            }
             while (x) {
-                // take up to KGRP active chunks; advance N -> f (fused)
-                uint64_t f[KGRP];
+                // take up to KGRP active chunks; advance N -> f (fused):
+                // all visited loads and N exchanges are issued together
+                uint64_t f[KGRP], vv[KGRP];
                 uint64_t bits = 0;
                 int nk = 0;
 #pragma unroll
@@ -309,20 +347,21 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                     nk += has;
                     bits |= (uint64_t)bt << (8 * k);
                     const bool ok = has && lane_ok && xw * 32u * p.cw + bt * p.cw + lane < p.nw;
-                    f[k] = ok ? ld_cg(p.N + rb + bt * p.cw) : 0ull;
+                    vv[k] = ok ? ld_cg(p.Vis + rb + bt * p.cw) : ~0ull;
+                    f[k] = ok ? 1ull : 0ull;
                 }
 #pragma unroll
                 for (int k = 0; k < KGRP; ++k) {
                     const uint32_t bt = (uint32_t)(bits >> (8 * k)) & 0xffu;
+                    if (f[k]) f[k] = atomicExch((unsigned long long *)(p.N + rb + bt * p.cw), 0ull);
+                }
+#pragma unroll
+                for (int k = 0; k < KGRP; ++k) {
+                    const uint32_t bt = (uint32_t)(bits >> (8 * k)) & 0xffu;
+                    f[k] &= ~vv[k];
                     if (f[k]) {
-                        uint64_t *np_ = p.N + rb + bt * p.cw;
-                        const uint64_t n = atomicExch((unsigned long long *)np_, 0ull);
-                        const uint64_t vis = ld_cg(p.Vis + rb + bt * p.cw);
-                        f[k] = n & ~vis;
-                        if (f[k]) {
-                            p.Vis[rb + bt * p.cw] = vis | f[k];
-                            if (STATS) st[S_WORD_ITEMS]++;
-                        }
+                        p.Vis[rb + bt * p.cw] = vv[k] | f[k];
+                        if (STATS) st[S_WORD_ITEMS]++;
                     }
                 }
                 bool anyk = false;
@@ -331,10 +370,16 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                 if (!__ballot_sync(0xffffffffu, anyk)) continue;
                 if (STATS && lane == 0) st[S_ITEMS]++;
                 int hslot = -1;
-                for (int t = A.toff[q]; t < A.toff[q + 1]; ++t) {
+                for (int t = t0; t < t0 + ntr; ++t) {
                     const int slot = A.tslot[t];
-                    const uint32_t *off = A.off[slot];
-                    const uint32_t beg = __ldg(off + v), end = __ldg(off + v + 1);
+                    uint32_t beg, end;
+                    if (t - t0 < 32) {
+                        beg = __shfl_sync(0xffffffffu, obeg, t - t0);
+                        end = __shfl_sync(0xffffffffu, oend, t - t0);
+                    } else {
+                        beg = __ldg(A.off[slot] + v);
+                        end = __ldg(A.off[slot] + v + 1);
+                    }
                     if (STATS && lane == 0) st[S_ITEM_TRANS]++;
                     if (end == beg) continue;
                     if (end - beg > HUB_EDGES) {
@@ -419,6 +464,8 @@ __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const 
         ctrl->active[1] = 0;
         ctrl->nhub_items = 0;
         ctrl->nhub_recs = 0;
+        ctrl->ucnt[0] = ctrl->ucnt[1] = 0;
+        ctrl->ucur[0] = ctrl->ucur[1] = 0;
     }
 }
 
@@ -681,7 +728,7 @@ struct LevelGraph {
 
 template <bool STATS>
 cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg, const LevelArgs &P0,
-                              const LevelArgs &P1, int grid, int hgrid) {
+                              const LevelArgs &P1, int grid, int hgrid, uint64_t nxbwords) {
     cudaError_t e;
     if ((e = cudaGraphCreate(&LG.g, 0)) != cudaSuccess) return e;
     cudaGraphConditionalHandle h;
@@ -711,14 +758,17 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
     const Layout *sg = Sg;
     LevelArgs p0 = P0, p1 = P1;
     Ctrl *ctrl = P0.ctrl;
-    int par0 = 0, par1 = 1;
+    uint64_t nxb = nxbwords;
     void *a0[] = {&a, &sg, &p0};
     void *a1[] = {&a, &sg, &p1};
-    void *m0[] = {&ctrl, &par0};
-    void *m1[] = {&ctrl, &par1, &h};
+    void *u0[] = {&p0, &nxb};
+    void *u1[] = {&p1, &nxb};
+    void *m1[] = {&ctrl, &h};
+    const int ugrid = (int)std::min<uint64_t>(148 * 4, (nxbwords + 255) / 256 + 1);
+    if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u0)) != cudaSuccess) return e;
     if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a0)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
-    if ((e = add((void *)k_level_mid, dim3(1), dim3(1), m0)) != cudaSuccess) return e;
+    if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_end, dim3(1), dim3(1), m1)) != cudaSuccess) return e;
@@ -728,10 +778,13 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
 // Level loop, host-driven (RPQ_HOST_LOOP=1, or if graph creation fails):
 // one flag readback per level.
 rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &P0, const LevelArgs &P1, int grid,
-                           int hgrid, cudaStream_t s, bool stats, uint32_t *h_flag, rpq_stats *out_stats) {
+                           int hgrid, uint64_t nxbwords, cudaStream_t s, bool stats, uint32_t *h_flag,
+                           rpq_stats *out_stats) {
     int par = 0;
+    const int ugrid = (int)std::min<uint64_t>(148 * 4, (nxbwords + 255) / 256 + 1);
     for (;;) {
         const LevelArgs &P = par ? P1 : P0;
+        k_units<<<ugrid, 256, 0, s>>>(P, nxbwords);
         if (stats) {
             k_level<true><<<grid, 256, 0, s>>>(A, Sg, P);
             k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
@@ -740,7 +793,6 @@ rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &
             k_level_hub<false><<<hgrid, 256, 0, s>>>(A, Sg, P);
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(h_flag, &P.ctrl->active[par ^ 1], 4, cudaMemcpyDeviceToHost, s));
-        k_level_mid<<<1, 1, 0, s>>>(P.ctrl, par);
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
         RPQ_CUDA_TRY(cudaGetLastError());
         out_stats->kernel_launches += 3;
@@ -954,7 +1006,8 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
 
     // ---- level loop setup: parity-0/1 argument sets and the device graph ----
     Layout *d_layout = (Layout *)ws.get(sizeof(Layout));
-    if (!d_layout) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+    uint32_t *ulist = (uint32_t *)ws.get(((nxwords + 31) / 32 + 1) * 4);
+    if (!d_layout || !ulist) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
     LevelArgs P0{}, P1{};
     P0.N = N; P0.Vis = Vis;
     P0.Xcur = X0; P0.Xnext = X1; P0.XBcur = XB0; P0.XBnext = XB1;
@@ -964,16 +1017,17 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     P0.hitem_cap = hitem_cap; P0.hrec_cap = hrec_cap;
     P0.nw = (uint32_t)nw; P0.nxw = (uint32_t)nxw; P0.cw = CW;
     P0.stats = d_stats;
+    P0.ulist = ulist;
     P1 = P0;
     P1.par = 1;
     std::swap(P1.Xcur, P1.Xnext);
     std::swap(P1.XBcur, P1.XBnext);
-    const int lgrid = grid_for(((nxwords + 31) / 32) * 32, 256, 148 * RPQ_LEVEL_MINB);
+    const int lgrid = 148 * RPQ_LEVEL_MINB;   // persistent: warps fetch work units dynamically
     const int hgrid = 148 * RPQ_LEVEL_MINB;
     LevelGraph LG;
     if (nbatches && !getenv("RPQ_HOST_LOOP")) {
-        cudaError_t ge = stats ? build_level_graph<true>(LG, A, d_layout, P0, P1, lgrid, hgrid)
-                               : build_level_graph<false>(LG, A, d_layout, P0, P1, lgrid, hgrid);
+        cudaError_t ge = stats ? build_level_graph<true>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords)
+                               : build_level_graph<false>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords);
         if (ge != cudaSuccess) {   // fall back to the host-driven loop
             cudaGetLastError();
             if (LG.exec) cudaGraphExecDestroy(LG.exec);
@@ -1040,7 +1094,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
             cudaError_t ge = cudaGraphLaunch(LG.exec, s);
             if (ge != cudaSuccess) st = rpq_fail(RPQ_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(ge));
         } else {
-            st = run_levels_host(A, d_layout, P0, P1, lgrid, hgrid, s, stats, h_cnt, &ST);
+            st = run_levels_host(A, d_layout, P0, P1, lgrid, hgrid, xbwords, s, stats, h_cnt, &ST);
         }
         if (timeit) {
             cudaEventRecord(evt1, s);
@@ -1171,7 +1225,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
         ST.levels = hc.levels;
-        if (LG.exec) ST.kernel_launches += 3ull * hc.levels;
+        if (LG.exec) ST.kernel_launches += 3ull * hc.levels + (hc.levels + 1) / 2;
         ST.expand_launches = 2ull * ST.levels;
     }
     if (stats) {
