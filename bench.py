@@ -144,39 +144,46 @@ def run_ours(args):
     queries = wl["queries"]
 
     # batch width: one batch per rank for N > 1 (round-robin sharding)
-    probe = {}
-    for rx in queries:
-        a = R.rpq_compile(G, rx)
-        r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=sp, batch_sources=args.batch)
-        probe[rx] = r.stats()
     bsz = {}
     for rx in queries:
-        P = probe[rx]["productive_sources"]
+        a = R.rpq_compile(G, rx)
+        P = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT, stream=sp).stats()["productive_sources"]
         if args.batch:
             bsz[rx] = args.batch
         elif world > 1:
             bsz[rx] = int(-(-P // world) + 63) // 64 * 64
         else:
             bsz[rx] = 0
+    # per-rank probe with the in-kernel counters (RPQ_STATS): PE and the
+    # algorithmic bytes of this rank's shard
+    probe = {}
+    for rx in queries:
+        a = R.rpq_compile(G, rx)
+        r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=sp, batch_sources=bsz[rx],
+                                shard_index=rank, shard_count=world)
+        probe[rx] = r.stats()
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")   # > 126 MB L2
 
     def step(mode):
-        tot = {"count": 0, "pe": 0, "launches": 0, "expand_ms": 0.0, "bytes": 0, "expand_launches": 0}
+        tot = {"count": 0, "pe": 0, "launches": 0, "expand_ms": 0.0, "levels": 0}
         for rx in queries:
             a = R.rpq_compile(G, rx)
             r = R.rpq_eval_allpairs(G, a, mode=mode, stream=sp, batch_sources=bsz[rx],
                                     shard_index=rank, shard_count=world)
             st = r.stats()
             tot["count"] += r.count
-            tot["pe"] += st["product_edges"]
             tot["launches"] += st["kernel_launches"]
             tot["expand_ms"] += st["expand_ms"]
-            tot["expand_launches"] += st["expand_launches"]
-            tot["bytes"] += algorithmic_bytes(st)
+            tot["levels"] += st["levels"]
         return tot
 
-    mode = R.RPQ_COUNT | R.RPQ_STATS | R.RPQ_TIME_KERNELS
+    # timed steps run without the in-kernel counters; the algorithmic bytes
+    # of a step come from the RPQ_STATS probe runs above (per query)
+    mode = R.RPQ_COUNT | R.RPQ_TIME_KERNELS
+    probe_bytes = sum(algorithmic_bytes(probe[rx]) for rx in queries)
+    probe_levels = sum(probe[rx]["levels"] for rx in queries)
+    probe_pe = sum(probe[rx]["product_edges"] for rx in queries)
     for _ in range(args.warmup):
         step(mode)
     ev0 = torch.cuda.Event(enable_timing=True)
@@ -203,7 +210,7 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     total_ms = float(sum(times))
-    pe_total = agg["pe"]
+    pe_total = probe_pe * args.steps          # PE is a property of (graph, query, shard)
     if world > 1:
         tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -252,8 +259,9 @@ def run_ours(args):
     pe_per_step = pe_total / args.steps
     value = pe_total / (total_ms / 1e3)
     peak, peak_src = load_peaks()
-    achieved = agg["bytes"] / (agg["expand_ms"] / 1e3) / 1e9 if agg["expand_ms"] > 0 else None
-    per_launch = agg["bytes"] / max(1, agg["expand_launches"])
+    step_bytes = probe_bytes * args.steps
+    achieved = step_bytes / (agg["expand_ms"] / 1e3) / 1e9 if agg["expand_ms"] > 0 else None
+    per_launch = probe_bytes / max(1, probe_levels)
     traffic = load_traffic()
     line = {
         "metric": "all-pairs RPQ product-edges traversed/s",
@@ -273,11 +281,13 @@ def run_ours(args):
                    "batch_sources": {rx: probe[rx]["batch_sources"] if not bsz[rx] else bsz[rx] for rx in queries},
                    "parallelism": f"source-batch shards x{world}",
                    "l2": "flushed between timed steps (256 MiB write)"},
-        "roofline": {"bound": "hbm", "kernel": "k_level (+k_level_hub)", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k_level (level loop: k_units + k_level + k_level_hub)",
+                     "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
                      "algorithmic_bytes_per_launch": per_launch,
-                     "launches": agg["expand_launches"],
+                     "launches": agg["levels"],
+                     "level_loop_ms_per_step": agg["expand_ms"] / args.steps,
                      "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                      "traffic_source": traffic.get("source") if traffic else None},
         "e2e": {"value": pe_per_step / (e2e_step / 1e3), "unit": "PE/s", "ms_per_step": e2e_step,

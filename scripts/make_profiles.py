@@ -1,0 +1,63 @@
+"""Turn the ncu captures brought back in gpurun_out/ into the committed
+summaries under profiles/ (run here, on the CPU box).
+
+usage: python scripts/make_profiles.py <round tag> <launches.csv> <traffic.csv> <full.ncu-rep>
+"""
+import csv, json, os, shutil, subprocess, sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "scripts"))
+import ncu_summary as S  # noqa: E402
+
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread", "launch__grid_size", "launch__occupancy_limit_registers",
+        "lts__t_sectors_srcunit_tex_op_read.sum", "lts__t_sectors_srcunit_tex_op_red.sum",
+        "lts__t_sectors_srcunit_tex_op_atom.sum", "lts__t_sectors_srcunit_tex_op_write.sum",
+        "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
+        "smsp__pcsamp_warps_issue_stalled_long_scoreboard", "smsp__pcsamp_warps_issue_stalled_wait",
+        "smsp__pcsamp_warps_issue_stalled_short_scoreboard", "smsp__pcsamp_warps_issue_stalled_selected"]
+
+
+def summarise(kind, path):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), kind, path],
+                         capture_output=True, text=True, check=True).stdout
+    return json.loads(out)
+
+
+def main():
+    tag, launches, traffic, rep = sys.argv[1:5]
+    pdir = os.path.join(ROOT, "profiles")
+    os.makedirs(pdir, exist_ok=True)
+    L = summarise("launches", launches)
+    with open(os.path.join(pdir, f"{tag}_launches_cfg2.json"), "w") as f:
+        json.dump(L, f, indent=1)
+    shutil.copy(launches, os.path.join(pdir, f"{tag}_launches_cfg2.csv"))
+    T = summarise("traffic", traffic)
+    k = T["k_level"]
+    with open(os.path.join(pdir, "traffic_cfg2.json"), "w") as f:
+        json.dump({"kernel": "k_level", "dram_bytes_per_launch": k["dram_bytes_per_launch"],
+                   "launches": k["launches"], "round": tag,
+                   "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
+                             "-k regex:k_level over one COUNT evaluation of each cfg2 query "
+                             "(scripts/prof_cfg2.py, RPQ_HOST_LOOP=1, PROF_NOSTATS=1)",
+                   "all": T}, f, indent=1)
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    h, u = rows[0], rows[1]
+    lines = []
+    for row in rows[2:]:
+        name = row[h.index("Kernel Name")]
+        lines.append(f"kernel: {name}")
+        for i, n in enumerate(h):
+            if n in KEYS:
+                lines.append(f"  {n:60s} {row[i]:>20s} {u[i]}")
+    with open(os.path.join(pdir, f"{tag}_k_level_full.txt"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    shutil.copy(rep, os.path.join(pdir, f"{tag}_k_level.ncu-rep"))
+    print(open(os.path.join(pdir, f"{tag}_k_level_full.txt")).read())
+
+
+if __name__ == "__main__":
+    main()

@@ -20,8 +20,9 @@ def kname(s):
 
 def to_unit(v, unit):
     v = float(v.replace(",", ""))
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
-             "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+             "second": 1e6, "s": 1e6, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+             "B": 1.0, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     return v * scale.get(unit, 1.0)
 
 

@@ -11,7 +11,8 @@ s = torch.cuda.current_stream().cuda_stream
 G = R.rpq_graph_load(g, stream=s)
 for rx in queries:
     a = R.rpq_compile(G, rx)
-    r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, batch_sources=B, stream=s)
+    mode = R.RPQ_COUNT if os.environ.get("PROF_NOSTATS") else R.RPQ_COUNT | R.RPQ_STATS
+    r = R.rpq_eval_allpairs(G, a, mode=mode, batch_sources=B, stream=s)
     torch.cuda.synchronize()
     st = r.stats()
     print(rx, r.count, st["levels"], st["product_edges"], st["word_items"], st["item_transitions"],
