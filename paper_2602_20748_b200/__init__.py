@@ -417,3 +417,18 @@ def rpq_result_source_counts(r: Result):
 
 def rpq_result_device_view(r: Result):
     return r.device_view()
+
+
+def crpq(g: Graph, vars, atoms, var_label=None, var_const=None, distinct=(), **kw) -> Result:
+    """Convenience marshalling for crpq_eval: vars = names; atoms = (x, regex,
+    y) with variable names; var_label = {var: vertex-label name};
+    var_const = {var: vertex id}; distinct = [(var, var)]."""
+    idx = {v: i for i, v in enumerate(vars)}
+    vl = [-1] * len(vars)
+    for v, name in (var_label or {}).items():
+        vl[idx[v]] = g.vertex_label_names.index(name)
+    vc = [-1] * len(vars)
+    for v, c in (var_const or {}).items():
+        vc[idx[v]] = int(c)
+    at = [(idx[x], rpq_compile(g, rx), idx[y]) for (x, rx, y) in atoms]
+    return crpq_eval(g, vl, vc, at, [(idx[a], idx[b]) for a, b in distinct], **kw)

@@ -1,9 +1,473 @@
-// crpq_eval: placeholder until the CRPQ join lands.
+// crpq_eval: conjunctive RPQs (Definition 2).
+//
+// A CRPQ is answered by "evaluating each RPQ atom and then combining the
+// results using joins".  Here:
+//   1. plan: order the atoms so that each one after the first shares a
+//      variable with the bound set (atoms with a constant endpoint first);
+//      a variable in no atom or a disconnected pattern is rejected
+//      (EUNSUPPORTED, reading R18);
+//   2. each atom x -rho-> y is evaluated by the RPQ kernels from the sources
+//      its x can take: the distinct values already bound to x, else the
+//      candidates of x (constant / vertex label condition (1) / all of V);
+//      its pairs are filtered by y's candidates (and s == d when x == y);
+//   3. the relation is joined with the table of bound tuples on the device:
+//      expansion by binary search over the (src,dst)-sorted relation when
+//      one endpoint is bound (the relation is re-sorted by (dst,src) when only
+//      y is), semi-join when both are;
+//   4. distinct-vertex filters, then a stable LSD radix sort gives
+//      tuples in lexicographic variable order.  Tuples are distinct because
+//      every relation is a set and each join step extends an assignment.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <vector>
+
 #include "internal.h"
 
-extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts,
+namespace {
+
+struct VarPred {
+    int64_t cst;               // -1 = free
+    int32_t label;             // -1 = any
+    const uint16_t *vlabel;
+    __device__ __forceinline__ bool ok(uint32_t v) const {
+        return (cst < 0 || (int64_t)v == cst) && (label < 0 || vlabel[v] == (uint16_t)label);
+    }
+};
+
+inline int grid_for(uint64_t n, int block = 256) {
+    uint64_t g = (n + block - 1) / block;
+    if (g > 148ull * 16) g = 148ull * 16;
+    return g ? (int)g : 1;
+}
+
+__global__ void k_cand_flags(VarPred p, uint32_t nv, uint8_t *flag) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x)
+        flag[v] = p.ok((uint32_t)v);
+}
+
+__global__ void k_pair_flags(const uint32_t *src, const uint32_t *dst, uint64_t n, VarPred py, int same,
+                             uint8_t *flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        flag[i] = py.ok(dst[i]) && (!same || src[i] == dst[i]);
+}
+
+__device__ __forceinline__ uint64_t lower_bound_u32(const uint32_t *a, uint64_t n, uint32_t key) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// rows of the table joined with a relation sorted by key column `rk`
+__global__ void k_join_count(const uint32_t *tkey, uint64_t nrows, const uint32_t *rk, uint64_t nrel,
+                             unsigned long long *lo, unsigned long long *cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nrows; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = tkey[i];
+        const uint64_t a = lower_bound_u32(rk, nrel, k);
+        const uint64_t b = lower_bound_u32(rk, nrel, k + 1) ;
+        lo[i] = a;
+        cnt[i] = (k == 0xffffffffu) ? (nrel - a) : (b - a);
+    }
+}
+
+__global__ void k_join_write(const uint32_t *const *tcols, uint32_t ncols, uint64_t nrows, const unsigned long long *lo,
+                             const unsigned long long *cnt, const unsigned long long *off, const uint32_t *rval,
+                             uint32_t *const *ocols) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nrows; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t c = cnt[i], o = off[i], l = lo[i];
+        for (uint64_t k = 0; k < c; ++k) {
+            for (uint32_t j = 0; j < ncols; ++j) ocols[j][o + k] = tcols[j][i];
+            ocols[ncols][o + k] = rval[l + k];
+        }
+    }
+}
+
+// both endpoints bound: keep rows whose (x, y) is in the (src,dst)-sorted relation
+__global__ void k_semijoin(const uint32_t *tx, const uint32_t *ty, uint64_t nrows, const uint32_t *rs,
+                           const uint32_t *rd, uint64_t nrel, uint8_t *flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nrows; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t x = tx[i], y = ty[i];
+        uint64_t a = lower_bound_u32(rs, nrel, x);
+        uint64_t b = (x == 0xffffffffu) ? nrel : lower_bound_u32(rs, nrel, x + 1);
+        while (a < b) {   // binary search of y in rd[a, b)
+            const uint64_t mid = (a + b) >> 1;
+            if (rd[mid] < y) a = mid + 1; else b = mid;
+        }
+        flag[i] = (a < nrel && rs[a] == x && rd[a] == y);
+    }
+}
+
+__global__ void k_ne_flags(const uint32_t *a, const uint32_t *b, uint64_t n, uint8_t *flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        flag[i] = flag[i] && a[i] != b[i];
+}
+
+__global__ void k_pack_swap(const uint32_t *s, const uint32_t *d, uint64_t n, uint64_t *key) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        key[i] = ((uint64_t)d[i] << 32) | s[i];
+}
+
+__global__ void k_unpack(const uint64_t *key, uint64_t n, uint32_t *hi, uint32_t *lo) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        hi[i] = (uint32_t)(key[i] >> 32);
+        lo[i] = (uint32_t)key[i];
+    }
+}
+
+__global__ void k_gather(const uint32_t *in, const uint32_t *idx, uint64_t n, uint32_t *out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = in[idx[i]];
+}
+
+__global__ void k_iota32(uint32_t *x, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        x[i] = (uint32_t)i;
+}
+
+// ---- host helpers ---------------------------------------------------------
+struct Pool {
+    cudaStream_t s;
+    std::vector<void *> ptrs;
+    ~Pool() { for (void *p : ptrs) dev_free(p, s); }
+    void *get(size_t b) {
+        void *p = dev_alloc(b ? b : 16, s);
+        if (p) ptrs.push_back(p);
+        return p;
+    }
+    void put(void *p) {
+        auto it = std::find(ptrs.begin(), ptrs.end(), p);
+        if (it != ptrs.end()) { dev_free(p, s); ptrs.erase(it); }
+    }
+};
+
+struct Table {
+    std::vector<uint32_t> vars;        // bound variables, column order
+    std::vector<uint32_t *> cols;      // device columns (Pool-owned)
+    uint64_t n = 0;
+    int col_of(uint32_t v) const {
+        for (size_t i = 0; i < vars.size(); ++i) if (vars[i] == v) return (int)i;
+        return -1;
+    }
+};
+
+// compact the columns of a table by a flag array
+rpq_status compact(Pool &P, std::vector<uint32_t *> &cols, uint64_t &n, const uint8_t *flag, cudaStream_t s) {
+    if (n == 0) return RPQ_OK;
+    uint64_t *d_n = (uint64_t *)P.get(8);
+    size_t tb = 0;
+    cub::DeviceSelect::Flagged(nullptr, tb, cols[0], flag, cols[0], d_n, (int64_t)n, s);
+    void *tmp = P.get(tb);
+    if (!d_n || !tmp) return rpq_fail(RPQ_ENOMEM, "crpq: out of device memory");
+    uint64_t m = 0;
+    for (auto &c : cols) {
+        uint32_t *o = (uint32_t *)P.get(n * 4);
+        if (!o) return rpq_fail(RPQ_ENOMEM, "crpq: out of device memory");
+        cub::DeviceSelect::Flagged(tmp, tb, c, flag, o, d_n, (int64_t)n, s);
+        P.put(c);
+        c = o;
+    }
+    RPQ_CUDA_TRY(cudaMemcpyAsync(&m, d_n, 8, cudaMemcpyDeviceToHost, s));
+    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    n = m;
+    return RPQ_OK;
+}
+
+void add_stats(rpq_stats &a, const rpq_stats &b) {
+    a.product_edges += b.product_edges;
+    a.word_items += b.word_items;
+    a.word_edge_ops += b.word_edge_ops;
+    a.items += b.items;
+    a.item_edges += b.item_edges;
+    a.item_transitions += b.item_transitions;
+    a.activations += b.activations;
+    a.next_reds += b.next_reds;
+    a.levels += b.levels;
+    a.batches += b.batches;
+    a.expand_launches += b.expand_launches;
+    a.kernel_launches += b.kernel_launches;
+    a.expand_ms += b.expand_ms;
+}
+
+}  // namespace
+
+extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts_in,
                                 rpq_result **out) {
-    (void)g; (void)q; (void)opts;
     if (out) *out = nullptr;
-    return rpq_fail(RPQ_EUNSUPPORTED, "crpq_eval: not built yet");
+    if (!g || !q || !out) return rpq_fail(RPQ_EINVAL, "crpq_eval: NULL argument");
+    const uint32_t nvars = q->num_vars, natoms = q->num_atoms;
+    if (nvars == 0 || nvars > RPQ_MAX_COLS) return rpq_fail(RPQ_EINVAL, "crpq_eval: 1..%d variables", RPQ_MAX_COLS);
+    if (natoms == 0 || !q->atom_x || !q->atom_y || !q->atom_nfa)
+        return rpq_fail(RPQ_EINVAL, "crpq_eval: no atoms");
+    std::vector<int32_t> vlab(nvars, -1);
+    std::vector<int64_t> vcst(nvars, -1);
+    for (uint32_t v = 0; v < nvars; ++v) {
+        if (q->var_label) vlab[v] = q->var_label[v];
+        if (q->var_const) vcst[v] = q->var_const[v];
+        if (vlab[v] >= 65536 || (vlab[v] >= 0 && !g->vlabel))
+            return rpq_fail(RPQ_EINVAL, "crpq_eval: variable %u has a vertex label but the graph has none", v);
+        if (vcst[v] >= (int64_t)g->nv) return rpq_fail(RPQ_EINVAL, "crpq_eval: constant >= |V|");
+    }
+    std::vector<int> used(nvars, 0);
+    for (uint32_t i = 0; i < natoms; ++i) {
+        if (q->atom_x[i] >= nvars || q->atom_y[i] >= nvars || !q->atom_nfa[i])
+            return rpq_fail(RPQ_EINVAL, "crpq_eval: bad atom %u", i);
+        used[q->atom_x[i]] = used[q->atom_y[i]] = 1;
+    }
+    for (uint32_t v = 0; v < nvars; ++v)
+        if (!used[v]) return rpq_fail(RPQ_EUNSUPPORTED, "crpq_eval: variable %u occurs in no atom (R18)", v);
+    for (uint32_t i = 0; i < q->num_distinct; ++i)
+        if (!q->distinct_pairs || q->distinct_pairs[2 * i] >= nvars || q->distinct_pairs[2 * i + 1] >= nvars)
+            return rpq_fail(RPQ_EINVAL, "crpq_eval: bad distinct filter");
+
+    // ---- plan: constants first, then atoms sharing a bound variable -------
+    std::vector<uint32_t> order;
+    std::vector<int> done(natoms, 0), bound(nvars, 0);
+    auto score = [&](uint32_t i) {
+        const uint32_t x = q->atom_x[i], y = q->atom_y[i];
+        int s = 0;
+        if (vcst[x] >= 0 || vcst[y] >= 0) s += 8;
+        if (bound[x]) s += 4;
+        if (bound[y]) s += 2;
+        if (vlab[x] >= 0) s += 1;
+        return s;
+    };
+    for (uint32_t k = 0; k < natoms; ++k) {
+        int best = -1, bs = -1;
+        for (uint32_t i = 0; i < natoms; ++i) {
+            if (done[i]) continue;
+            const bool connected = k == 0 || bound[q->atom_x[i]] || bound[q->atom_y[i]];
+            if (!connected) continue;
+            const int sc = score(i);
+            if (sc > bs) { bs = sc; best = (int)i; }
+        }
+        if (best < 0) return rpq_fail(RPQ_EUNSUPPORTED, "crpq_eval: disconnected pattern (R18)");
+        done[best] = 1;
+        bound[q->atom_x[best]] = bound[q->atom_y[best]] = 1;
+        order.push_back((uint32_t)best);
+    }
+
+    rpq_eval_opts o{};
+    if (opts_in) o = *opts_in;
+    RPQ_CUDA_TRY(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)o.cuda_stream;
+    Pool P{s, {}};
+    rpq_stats ST{};
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+    auto pred = [&](uint32_t v) { return VarPred{vcst[v], vlab[v], g->vlabel}; };
+
+    Table T;
+    for (uint32_t k = 0; k < natoms; ++k) {
+        const uint32_t ai = order[k];
+        const uint32_t x = q->atom_x[ai], y = q->atom_y[ai];
+        const rpq_nfa *nfa = q->atom_nfa[ai];
+        const int cx = T.col_of(x), cy = T.col_of(y);
+        // ---- sources of the atom ----
+        uint32_t *srcs = nullptr;
+        uint64_t nsrc = 0;
+        bool all_v = false;
+        if (cx >= 0) {
+            // distinct values bound to x
+            uint32_t *tmpk = (uint32_t *)P.get(T.n * 4), *sorted = (uint32_t *)P.get(T.n * 4);
+            srcs = (uint32_t *)P.get(T.n * 4);
+            uint64_t *d_n = (uint64_t *)P.get(8);
+            if (!tmpk || !sorted || !srcs || !d_n) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            RPQ_CUDA_TRY(cudaMemcpyAsync(tmpk, T.cols[cx], T.n * 4, cudaMemcpyDeviceToDevice, s));
+            size_t t1 = 0, t2 = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, t1, tmpk, sorted, (int64_t)T.n, 0, 32, s);
+            cub::DeviceSelect::Unique(nullptr, t2, sorted, srcs, d_n, (int64_t)T.n, s);
+            void *tmp = P.get(std::max(t1, t2));
+            if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            cub::DeviceRadixSort::SortKeys(tmp, t1, tmpk, sorted, (int64_t)T.n, 0, 32, s);
+            cub::DeviceSelect::Unique(tmp, t2, sorted, srcs, d_n, (int64_t)T.n, s);
+            RPQ_CUDA_TRY(cudaMemcpyAsync(&nsrc, d_n, 8, cudaMemcpyDeviceToHost, s));
+            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        } else if (vcst[x] >= 0) {
+            srcs = (uint32_t *)P.get(4);
+            if (!srcs) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            const uint32_t c = (uint32_t)vcst[x];
+            RPQ_CUDA_TRY(cudaMemcpyAsync(srcs, &c, 4, cudaMemcpyHostToDevice, s));
+            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+            nsrc = 1;
+        } else if (vlab[x] >= 0) {
+            uint8_t *flag = (uint8_t *)P.get(g->nv);
+            srcs = (uint32_t *)P.get((uint64_t)g->nv * 4);
+            uint64_t *d_n = (uint64_t *)P.get(8);
+            if (!flag || !srcs || !d_n) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            k_cand_flags<<<grid_for(g->nv), 256, 0, s>>>(pred(x), g->nv, flag);
+            size_t tb = 0;
+            thrust::counting_iterator<uint32_t> it(0);
+            cub::DeviceSelect::Flagged(nullptr, tb, it, flag, srcs, d_n, (int64_t)g->nv, s);
+            void *tmp = P.get(tb);
+            if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            cub::DeviceSelect::Flagged(tmp, tb, it, flag, srcs, d_n, (int64_t)g->nv, s);
+            RPQ_CUDA_TRY(cudaMemcpyAsync(&nsrc, d_n, 8, cudaMemcpyDeviceToHost, s));
+            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        } else {
+            all_v = true;
+        }
+        // ---- evaluate the atom (sorted distinct pairs) ----
+        rpq_eval_opts ao = o;
+        ao.mode = RPQ_PAIRS | (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS));
+        ao.shard_index = 0;
+        ao.shard_count = 1;
+        rpq_result *rel = nullptr;
+        rpq_status st = all_v ? eval_sources_device(g, nfa, nullptr, 0, &ao, &rel)
+                              : eval_sources_device(g, nfa, srcs, nsrc, &ao, &rel);
+        if (st != RPQ_OK) return st;
+        add_stats(ST, rel->stats);
+        struct RelGuard { rpq_result *r; ~RelGuard() { rpq_result_release(r); } } rg{rel};
+        uint64_t nrel = rel->nrows;
+        std::vector<uint32_t *> rc = {rel->cols[0], rel->cols[1]};
+        // own the columns in the pool (so compaction can replace them)
+        for (auto &c : rc) {
+            uint32_t *o2 = (uint32_t *)P.get(std::max<uint64_t>(nrel, 1) * 4);
+            if (!o2) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            if (nrel) RPQ_CUDA_TRY(cudaMemcpyAsync(o2, c, nrel * 4, cudaMemcpyDeviceToDevice, s));
+            c = o2;
+        }
+        // ---- filter by y's candidates (and s == d for x == y) ----
+        if (nrel) {
+            uint8_t *flag = (uint8_t *)P.get(nrel);
+            if (!flag) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            k_pair_flags<<<grid_for(nrel), 256, 0, s>>>(rc[0], rc[1], nrel, pred(y), x == y ? 1 : 0, flag);
+            st = compact(P, rc, nrel, flag, s);
+            if (st != RPQ_OK) return st;
+        }
+        // ---- join ----
+        if (k == 0) {
+            T.vars = {x};
+            T.cols = {rc[0]};
+            if (y != x) { T.vars.push_back(y); T.cols.push_back(rc[1]); }
+            T.n = nrel;
+            continue;
+        }
+        if (cx >= 0 && cy >= 0) {   // semi-join (relation sorted by (src,dst))
+            if (T.n) {
+                uint8_t *flag = (uint8_t *)P.get(T.n);
+                if (!flag) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+                k_semijoin<<<grid_for(T.n), 256, 0, s>>>(T.cols[cx], T.cols[cy], T.n, rc[0], rc[1], nrel, flag);
+                st = compact(P, T.cols, T.n, flag, s);
+                if (st != RPQ_OK) return st;
+            }
+            continue;
+        }
+        // one endpoint bound: key column of the relation must be sorted
+        const bool by_src = cx >= 0;
+        uint32_t *rkey = rc[0], *rval = rc[1];
+        if (!by_src && nrel) {
+            uint64_t *k1 = (uint64_t *)P.get(nrel * 8), *k2 = (uint64_t *)P.get(nrel * 8);
+            if (!k1 || !k2) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            k_pack_swap<<<grid_for(nrel), 256, 0, s>>>(rc[0], rc[1], nrel, k1);
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tb, k1, k2, (int64_t)nrel, 0, 64, s);
+            void *tmp = P.get(tb);
+            if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            cub::DeviceRadixSort::SortKeys(tmp, tb, k1, k2, (int64_t)nrel, 0, 64, s);
+            k_unpack<<<grid_for(nrel), 256, 0, s>>>(k2, nrel, rc[1], rc[0]);   // rc[1] = dst (key), rc[0] = src
+            rkey = rc[1];
+            rval = rc[0];
+        }
+        const int ck = by_src ? cx : cy;
+        const uint32_t newvar = by_src ? y : x;
+        unsigned long long *lo = (unsigned long long *)P.get(std::max<uint64_t>(T.n, 1) * 8);
+        unsigned long long *cnt = (unsigned long long *)P.get(std::max<uint64_t>(T.n, 1) * 8);
+        unsigned long long *off = (unsigned long long *)P.get(std::max<uint64_t>(T.n, 1) * 8 + 8);
+        if (!lo || !cnt || !off) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+        uint64_t total = 0;
+        if (T.n) {
+            k_join_count<<<grid_for(T.n), 256, 0, s>>>(T.cols[ck], T.n, rkey, nrel, lo, cnt);
+            size_t tb = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int64_t)T.n, s);
+            void *tmp = P.get(tb);
+            if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int64_t)T.n, s);
+            unsigned long long a = 0, b = 0;
+            RPQ_CUDA_TRY(cudaMemcpyAsync(&a, off + T.n - 1, 8, cudaMemcpyDeviceToHost, s));
+            RPQ_CUDA_TRY(cudaMemcpyAsync(&b, cnt + T.n - 1, 8, cudaMemcpyDeviceToHost, s));
+            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+            total = a + b;
+        }
+        std::vector<uint32_t *> nc(T.cols.size() + 1);
+        for (auto &c : nc) {
+            c = (uint32_t *)P.get(std::max<uint64_t>(total, 1) * 4);
+            if (!c) return rpq_fail(RPQ_ENOMEM, "crpq: out of device memory (%llu tuples)", (unsigned long long)total);
+        }
+        if (total) {
+            uint32_t **d_in = (uint32_t **)P.get(T.cols.size() * sizeof(void *));
+            uint32_t **d_out = (uint32_t **)P.get(nc.size() * sizeof(void *));
+            if (!d_in || !d_out) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            RPQ_CUDA_TRY(cudaMemcpyAsync(d_in, T.cols.data(), T.cols.size() * sizeof(void *), cudaMemcpyHostToDevice, s));
+            RPQ_CUDA_TRY(cudaMemcpyAsync(d_out, nc.data(), nc.size() * sizeof(void *), cudaMemcpyHostToDevice, s));
+            k_join_write<<<grid_for(T.n), 256, 0, s>>>(d_in, (uint32_t)T.cols.size(), T.n, lo, cnt, off, rval, d_out);
+            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        for (auto c : T.cols) P.put(c);
+        T.cols = nc;
+        T.vars.push_back(newvar);
+        T.n = total;
+    }
+
+    // ---- distinct-vertex filters (CQ4/CQ5) ----
+    if (q->num_distinct && T.n) {
+        uint8_t *flag = (uint8_t *)P.get(T.n);
+        if (!flag) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+        RPQ_CUDA_TRY(cudaMemsetAsync(flag, 1, T.n, s));
+        for (uint32_t i = 0; i < q->num_distinct; ++i) {
+            const int a = T.col_of(q->distinct_pairs[2 * i]), b = T.col_of(q->distinct_pairs[2 * i + 1]);
+            k_ne_flags<<<grid_for(T.n), 256, 0, s>>>(T.cols[a], T.cols[b], T.n, flag);
+        }
+        rpq_status st = compact(P, T.cols, T.n, flag, s);
+        if (st != RPQ_OK) return st;
+    }
+
+    // ---- lexicographic order in variable order: stable LSD radix passes ----
+    rpq_result *res = new rpq_result();
+    res->device = g->device;
+    res->ncols = nvars;
+    res->nrows = T.n;
+    res->count = T.n;
+    auto fail = [&](rpq_status st) { rpq_result_release(res); return st; };
+    for (uint32_t v = 0; v < nvars; ++v) {
+        if (cudaMalloc(&res->cols[v], std::max<uint64_t>(T.n, 1) * 4) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(rpq_fail(RPQ_ENOMEM, "crpq: out of device memory (result)"));
+        }
+    }
+    if (T.n) {
+        uint32_t *perm = (uint32_t *)P.get(T.n * 4), *perm2 = (uint32_t *)P.get(T.n * 4);
+        uint32_t *key = (uint32_t *)P.get(T.n * 4), *key2 = (uint32_t *)P.get(T.n * 4);
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, key, key2, perm, perm2, (int64_t)T.n, 0, 32, s);
+        void *tmp = P.get(tb);
+        if (!perm || !perm2 || !key || !key2 || !tmp) return fail(rpq_fail(RPQ_ENOMEM, "crpq: oom"));
+        k_iota32<<<grid_for(T.n), 256, 0, s>>>(perm, T.n);
+        for (int v = (int)nvars - 1; v >= 0; --v) {
+            const int c = T.col_of((uint32_t)v);
+            k_gather<<<grid_for(T.n), 256, 0, s>>>(T.cols[c], perm, T.n, key);
+            cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, perm, perm2, (int64_t)T.n, 0, 32, s);
+            std::swap(perm, perm2);
+        }
+        for (uint32_t v = 0; v < nvars; ++v)
+            k_gather<<<grid_for(T.n), 256, 0, s>>>(T.cols[T.col_of(v)], perm, T.n, res->cols[v]);
+    }
+    cudaEventRecord(e1, s);
+    cudaError_t ce = cudaStreamSynchronize(s);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (ce != cudaSuccess) return fail(rpq_fail(RPQ_ECUDA, "crpq: %s", cudaGetErrorString(ce)));
+    ST.total_ms = ms;
+    ST.count = T.n;
+    res->stats = ST;
+    *out = res;
+    return RPQ_OK;
 }

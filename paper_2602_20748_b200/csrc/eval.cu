@@ -446,27 +446,65 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto
 }
 
 // Seed batch sources: source i of the batch gets bit i in N of row (q0, s_i)
-// and its chunk is marked active; the first level moves it into Vis.
+// and its chunk is marked active; the first level moves it into Vis.  With
+// `skip_q0` (q0 has no incoming transition and is not final, so its rows
+// would only ever hold the seeds) nothing is written here: k_seed_expand
+// expands the seeds directly and q0 gets no rows at all.
 __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const uint32_t *__restrict__ pidx,
                        uint64_t b0, uint32_t nb, uint64_t *N, uint32_t *X, uint32_t *XB, uint32_t nw, uint32_t nxw,
-                       uint32_t cw, Ctrl *ctrl) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
-        const uint32_t s = cand[pidx[b0 + i]];
-        const uint64_t row = S.row_base[0] + (s - S.lo[0]);
-        const uint32_t w = i >> 6, c = w / cw;
-        N[row * nw + w] = 1ull << (i & 63);          // rows are distinct: plain stores
-        const uint64_t xi = row * nxw + c / 32;
-        X[xi] = 1u << (c & 31);
-        atomicOr(XB + (xi >> 10), 1u << ((xi >> 5) & 31));
-    }
+                       uint32_t cw, Ctrl *ctrl, int skip_q0) {
+    if (!skip_q0)
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+            const uint32_t s = cand[pidx[b0 + i]];
+            const uint64_t row = S.row_base[0] + (s - S.lo[0]);
+            const uint32_t w = i >> 6, c = w / cw;
+            N[row * nw + w] = 1ull << (i & 63);          // rows are distinct: plain stores
+            const uint64_t xi = row * nxw + c / 32;
+            X[xi] = 1u << (c & 31);
+            atomicOr(XB + (xi >> 10), 1u << ((xi >> 5) & 31));
+        }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ctrl->active[0] = nb ? 1u : 0u;
+        ctrl->active[0] = (nb && !skip_q0) ? 1u : 0u;
         ctrl->active[1] = 0;
         ctrl->nhub_items = 0;
         ctrl->nhub_recs = 0;
         ctrl->ucnt[0] = ctrl->ucnt[1] = 0;
         ctrl->ucur[0] = ctrl->ucur[1] = 0;
     }
+}
+
+// Level 0 without q0 rows: a warp per batch source expands its single bit
+// along q0's transitions straight into N / X / XB of the parity-0 level.
+// p must be the parity-1 argument set (its "next" buffers are parity 0).
+template <bool STATS>
+__global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layout *__restrict__ Sg,
+                                                     const LevelArgs p, const uint32_t *__restrict__ cand,
+                                                     const uint32_t *__restrict__ pidx, uint64_t b0, uint32_t nb) {
+    __shared__ Layout S;
+    load_layout(S, Sg, A.nq);
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool act = false;
+    for (uint64_t i = wid; i < nb; i += nwarps) {
+        const uint32_t sv = cand[pidx[b0 + i]];
+        const uint32_t w = (uint32_t)(i >> 6), c = w / p.cw;
+        uint64_t f[KGRP] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (lane == (int)(w - c * p.cw)) f[0] = 1ull << (i & 63);
+        const uint64_t bits = c & 31u;
+        const uint32_t xw = c >> 5;
+        if (STATS && lane == 0) st[S_ITEMS]++;
+        for (int t = A.toff[0]; t < A.toff[1]; ++t) {
+            const int slot = A.tslot[t];
+            const uint32_t beg = __ldg(A.off[slot] + sv), end = __ldg(A.off[slot] + sv + 1);
+            if (STATS && lane == 0) st[S_ITEM_TRANS]++;
+            if (end > beg)
+                expand_edges<1, STATS>(p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act);
+        }
+    }
+    if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
+    flush_stats<STATS>(st, p.stats);
 }
 
 // ---- productive sources: s with an out-edge under a label leaving q0 ------
@@ -894,6 +932,13 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         in_range[a->to[t]] = hull(in_range[a->to[t]], Range{c.dst_min, c.dst_max});
     }
 
+    // q0 needs rows only if something can enter it or it is final (its row
+    // then carries the epsilon pair); otherwise level 0 expands the seeds
+    // directly (k_seed_expand)
+    bool q0_entered = false;
+    for (size_t t = 0; t < a->to.size(); ++t) q0_entered |= a->to[t] == 0;
+    const bool skip_q0 = a->nq > 0 && !q0_entered && !((a->final_mask >> 0) & 1ull) && !getenv("RPQ_NO_SKIP_Q0");
+
     // ---- batch plan -------------------------------------------------------
     // Rows of the worst batch (q0 range = hull of all productive sources) set
     // the word budget: 3 state arrays x 8 B + worklists/bitmaps per word.
@@ -908,7 +953,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     uint64_t R_max = 0;
     for (uint32_t q = 0; q < a->nq; ++q) {
         Range r = in_range[q];
-        if (q == 0 && np) r = hull(r, Range{p_first, p_last});
+        if (q == 0 && np && !skip_q0) r = hull(r, Range{p_first, p_last});
         R_max += r.empty() ? 0 : (uint64_t)r.hi - r.lo + 1;
     }
     size_t free_b = 0, total_b = 0;
@@ -1074,7 +1119,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         Range fin_hull{1, 0};
         for (uint32_t q = 0; q < a->nq; ++q) {
             Range r = in_range[q];
-            if (q == 0) r = hull(r, Range{s_first, s_last});
+            if (q == 0 && !skip_q0) r = hull(r, Range{s_first, s_last});
             S.row_base[q] = rows;
             S.lo[q] = r.empty() ? 0 : r.lo;
             S.len[q] = r.empty() ? 0 : r.hi - r.lo + 1;
@@ -1085,8 +1130,15 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
             RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, &S, sizeof(Layout), cudaMemcpyHostToDevice, s));
-        k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, N, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl);
+        k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, N, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl,
+                                            skip_q0 ? 1 : 0);
         ST.kernel_launches++;
+        if (skip_q0) {
+            const int sg = grid_for((uint64_t)nb * 32, 256, 148 * 8);
+            if (stats) k_seed_expand<true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
+            else k_seed_expand<false><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
+            ST.kernel_launches++;
+        }
         PT.mark("seed");
         rpq_status st = RPQ_OK;
         if (timeit) cudaEventRecord(evt0, s);
