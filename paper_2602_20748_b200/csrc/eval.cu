@@ -98,7 +98,8 @@ struct Ctrl {                  // per-level device counters / flags
     uint32_t levels;           // levels run (device-side loop)
     uint32_t ucnt[2];          // active work units listed for the level of each parity
     uint32_t ucur[2];          // work-unit cursor (dynamic fetch) per parity
-    uint32_t pad[3];
+    uint32_t ntouched;         // entries of LevelArgs::TL
+    uint32_t pad[2];
 };
 
 // One BFS level over the rows whose activity bit is set in (Xcur, XBcur).
@@ -121,6 +122,9 @@ struct LevelArgs {
     uint32_t nxw;              // X words per row
     uint32_t cw;               // words per chunk (power of two <= 32)
     uint32_t *ulist;           // active work units of the level (k_units)
+    uint32_t *TX;              // OR of all consumed X words of the batch (touched chunks)
+    uint32_t *TU;              // touched work units of the batch (bitmap) ...
+    uint32_t *TL;              // ... and their list (ctrl->ntouched entries)
     unsigned long long *stats;
 };
 
@@ -148,6 +152,12 @@ __device__ __forceinline__ void load_layout(Layout &S, const Layout *__restrict_
     __syncthreads();
 }
 
+__device__ __forceinline__ int row_state(const Layout &S, uint32_t nq, uint64_t row) {
+    int q = 0;
+    while (q + 1 < (int)nq && S.row_base[q + 1] <= row) ++q;
+    return q;
+}
+
 // Before every level: list the active work units (set bits of XBcur, one
 // unit = 32 X words) for dynamic fetching, clear XBcur, and reset the
 // counters of the other parity / the hub buffers.  Block 0 does the resets.
@@ -167,35 +177,124 @@ __global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
         const uint64_t w = w0 + lane;
         uint32_t x = w < nxbwords ? __ldcg(p.XBcur + w) : 0u;
         if (x) p.XBcur[w] = 0u;
+        // units seen for the first time in this batch -> touched list (the
+        // TU word w holds exactly the units of XB word w: one owner here)
+        uint32_t fresh = 0;
+        if (x) {
+            const uint32_t tu = p.TU[w];
+            fresh = x & ~tu;
+            if (fresh) p.TU[w] = tu | fresh;
+        }
         const int c = __popc(x);
-        int incl = c;
+        const int cf = __popc(fresh);
+        int incl = c, inclf = cf;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            const int yf = __shfl_up_sync(0xffffffffu, inclf, o);
+            if (lane >= o) { incl += y; inclf += yf; }
         }
         const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        const int totf = __shfl_sync(0xffffffffu, inclf, 31);
         if (!tot) continue;
-        uint32_t base = 0;
-        if (lane == 31) base = atomicAdd(&p.ctrl->ucnt[par], (uint32_t)tot);
+        uint32_t base = 0, basef = 0;
+        if (lane == 31) {
+            base = atomicAdd(&p.ctrl->ucnt[par], (uint32_t)tot);
+            if (totf) basef = atomicAdd(&p.ctrl->ntouched, (uint32_t)totf);
+        }
         base = __shfl_sync(0xffffffffu, base, 31) + (uint32_t)(incl - c);
+        basef = __shfl_sync(0xffffffffu, basef, 31) + (uint32_t)(inclf - cf);
         while (x) {
             const int b = __ffs(x) - 1;
             x &= x - 1;
             p.ulist[base++] = (uint32_t)(w * 32 + b);
         }
+        while (fresh) {
+            const int b = __ffs(fresh) - 1;
+            fresh &= fresh - 1;
+            p.TL[basef++] = (uint32_t)(w * 32 + b);
+        }
     }
+}
+
+// ---- touched-set maintenance (sparse batches) ------------------------------
+// A warp per touched unit (32 X words): zero the visited words of every
+// chunk the batch touched, and the touched bitmaps, so the next batch starts
+// clean without a dense memset of the whole state.
+__global__ void k_clear_touched(const LevelArgs p, uint32_t ntl) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    for (uint64_t t = wid; t < ntl; t += nwarps) {
+        const uint64_t u = p.TL[t];
+        const uint64_t xi_l = u * 32 + lane;
+        const uint32_t tx = xi_l < p.nxwords ? p.TX[xi_l] : 0u;
+        if (tx) p.TX[xi_l] = 0u;
+        if (lane == 0) p.TU[u >> 5] = 0u;
+        unsigned todo = __ballot_sync(0xffffffffu, tx != 0);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            uint32_t x = __shfl_sync(0xffffffffu, tx, src);
+            const uint64_t xi = u * 32 + src;
+            const uint64_t row = xi / p.nxw;
+            const uint32_t xw = (uint32_t)(xi % p.nxw);
+            while (x) {
+                const uint32_t bt = (uint32_t)(__ffs(x) - 1);
+                x &= x - 1;
+                const uint64_t col = (uint64_t)(xw * 32u + bt) * p.cw + lane;
+                if (lane < (int)p.cw && col < p.nw) p.Vis[row * p.nw + col] = 0ull;
+            }
+        }
+    }
+}
+
+// COUNT over the touched chunks only: bits of Vis[q][v][w] for final q that
+// are not already set in a lower-numbered final state's row of v (the OR over
+// final states, counted once).
+__global__ void k_count_touched(const DevAuto A, const Layout S, const LevelArgs p, uint32_t ntl,
+                                unsigned long long *total) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    unsigned long long acc = 0;
+    for (uint64_t t = wid; t < ntl; t += nwarps) {
+        const uint64_t u = p.TL[t];
+        const uint64_t xi_l = u * 32 + lane;
+        const uint32_t tx = xi_l < p.nxwords ? p.TX[xi_l] : 0u;
+        unsigned todo = __ballot_sync(0xffffffffu, tx != 0);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            uint32_t x = __shfl_sync(0xffffffffu, tx, src);
+            const uint64_t xi = u * 32 + src;
+            const uint64_t row = xi / p.nxw;
+            const uint32_t xw = (uint32_t)(xi % p.nxw);
+            const int q = row_state(S, A.nq, row);
+            if (!((A.final_mask >> q) & 1ull)) continue;
+            const uint32_t v = S.lo[q] + (uint32_t)(row - S.row_base[q]);
+            while (x) {
+                const uint32_t bt = (uint32_t)(__ffs(x) - 1);
+                x &= x - 1;
+                const uint64_t col = (uint64_t)(xw * 32u + bt) * p.cw + lane;
+                if (lane >= (int)p.cw || col >= p.nw) continue;
+                uint64_t w = ld_cg(p.Vis + row * p.nw + col);
+                for (int f = 0; f < q && w; ++f)
+                    if (((A.final_mask >> f) & 1ull) && v - S.lo[f] < S.len[f])
+                        w &= ~ld_cg(p.Vis + (S.row_base[f] + (v - S.lo[f])) * p.nw + col);
+                acc += __popcll(w);
+            }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0 && acc) atomicAdd(total, acc);
 }
 
 __global__ void k_level_end(Ctrl *ctrl, cudaGraphConditionalHandle h) {
     cudaGraphSetConditional(h, ctrl->active[0] ? 1u : 0u);   // activations of the parity-1 level
 }
 
-__device__ __forceinline__ int row_state(const Layout &S, uint32_t nq, uint64_t row) {
-    int q = 0;
-    while (q + 1 < (int)nq && S.row_base[q + 1] <= row) ++q;
-    return q;
-}
 
 // Expand the edges [beg, end) of one CSR row for a group of up to KGRP
 // active chunks of X word xw (chunk positions packed 8 bits each in `bits`).
@@ -311,7 +410,10 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
         const uint64_t u = p.ulist[ui];
         const uint64_t xi_l = u * 32 + lane;
         const uint32_t xl = xi_l < p.nxwords ? __ldcg(p.Xcur + xi_l) : 0u;
-        if (xl) p.Xcur[xi_l] = 0u;
+        if (xl) {
+            p.Xcur[xi_l] = 0u;
+            p.TX[xi_l] |= xl;          // single owner per level; levels are ordered
+        }
         unsigned todo = __ballot_sync(0xffffffffu, xl != 0);
         while (todo) {
             const int src = __ffs(todo) - 1;
@@ -470,6 +572,7 @@ __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const 
         ctrl->nhub_recs = 0;
         ctrl->ucnt[0] = ctrl->ucnt[1] = 0;
         ctrl->ucur[0] = ctrl->ucur[1] = 0;
+        ctrl->ntouched = 0;
     }
 }
 
@@ -1051,8 +1154,16 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
 
     // ---- level loop setup: parity-0/1 argument sets and the device graph ----
     Layout *d_layout = (Layout *)ws.get(sizeof(Layout));
-    uint32_t *ulist = (uint32_t *)ws.get(((nxwords + 31) / 32 + 1) * 4);
-    if (!d_layout || !ulist) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+    const uint64_t nunits = (nxwords + 31) / 32;
+    uint32_t *ulist = (uint32_t *)ws.get((nunits + 1) * 4);
+    uint32_t *TX = (uint32_t *)ws.get(nxwords * 4 + 128);
+    uint32_t *TU = (uint32_t *)ws.get(((nunits + 31) / 32 + 1) * 4);
+    uint32_t *TL = (uint32_t *)ws.get((nunits + 1) * 4);
+    if (!d_layout || !ulist || !TX || !TU || !TL) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+    if (nbatches) {
+        RPQ_CUDA_TRY(cudaMemsetAsync(TX, 0, nxwords * 4 + 128, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(TU, 0, ((nunits + 31) / 32 + 1) * 4, s));
+    }
     LevelArgs P0{}, P1{};
     P0.N = N; P0.Vis = Vis;
     P0.Xcur = X0; P0.Xnext = X1; P0.XBcur = XB0; P0.XBnext = XB1;
@@ -1063,6 +1174,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     P0.nw = (uint32_t)nw; P0.nxw = (uint32_t)nxw; P0.cw = CW;
     P0.stats = d_stats;
     P0.ulist = ulist;
+    P0.TX = TX; P0.TU = TU; P0.TL = TL;
     P1 = P0;
     P1.par = 1;
     std::swap(P1.Xcur, P1.Xnext);
@@ -1081,6 +1193,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     }
     PT.mark("level graph");
 
+    uint32_t prev_touched = 0;   // touched units of the previous batch of this shard
     for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count) {
         const uint64_t jlo = jstart(b), jhi = (b + 1 < nb_eff) ? jstart(b + 1) : nsrc;
         ST.batches++;
@@ -1127,7 +1240,14 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
             if ((a->final_mask >> q) & 1) fin_hull = hull(fin_hull, r);
         }
         if (b != (uint64_t)o.shard_index) {   // visited words of the previous batch
-            RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
+            if ((uint64_t)prev_touched * 4 > nunits) {
+                RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
+                RPQ_CUDA_TRY(cudaMemsetAsync(TX, 0, nxwords * 4 + 128, s));
+                RPQ_CUDA_TRY(cudaMemsetAsync(TU, 0, ((nunits + 31) / 32 + 1) * 4, s));
+            } else if (prev_touched) {
+                k_clear_touched<<<grid_for((uint64_t)prev_touched * 32), 256, 0, s>>>(P0, prev_touched);
+                ST.kernel_launches++;
+            }
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, &S, sizeof(Layout), cudaMemcpyHostToDevice, s));
         k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, N, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl,
@@ -1162,9 +1282,17 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         const uint32_t vlo = fin_hull.empty() ? 0 : fin_hull.lo;
         const uint64_t vn = fin_hull.empty() ? 0 : (uint64_t)fin_hull.hi - fin_hull.lo + 1;
         const uint64_t eps_np = eps ? (jhi - jlo) - nb : 0;   // non-productive candidates in the interval
+        RPQ_CUDA_TRY(cudaMemcpyAsync(h_cnt + 4, &ctrl->ntouched, 4, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        prev_touched = h_cnt[4];
+        const bool sparse = (uint64_t)prev_touched * 4 <= nunits;
         if (!want_ps) {
             RPQ_CUDA_TRY(cudaMemsetAsync(d_total, 0, 8, s));
-            if (vn) {
+            if (sparse && prev_touched) {
+                k_count_touched<<<grid_for((uint64_t)prev_touched * 32), 256, 0, s>>>(A, S, P0, prev_touched,
+                                                                                    d_total);
+                ST.kernel_launches++;
+            } else if (vn) {
                 k_count_total<<<grid_for(vn * nw), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, d_total);
                 ST.kernel_launches++;
             }

@@ -234,3 +234,123 @@ def sample_sources(num_vertices: int, n: int, seed: int) -> np.ndarray:
     rng = np.random.default_rng(seed)
     n = min(n, num_vertices)
     return np.sort(rng.choice(num_vertices, n, replace=False)).astype(np.uint32)
+
+
+# --------------------------------------------------------------------------
+# cfg3 / cfg4: LDBC-SNB-shaped social graph
+# --------------------------------------------------------------------------
+LDBC_VERTEX_LABELS = ["Person", "Forum", "Post", "Comment", "Tag", "TagClass", "City", "Country",
+                      "Continent", "University", "Company", "Filler"]
+LDBC_EDGE_LABELS = ["knows", "replyOf", "hasCreator", "hasTag", "containerOf", "isLocatedIn", "hasMember",
+                    "hasModerator", "hasInterest", "studyAt", "workAt", "isPartOf", "isSubclassOf", "hasType",
+                    "likes"]
+# SF10 sizes: |V| = 35.5 M and |E| = 219.4 M, 12 vertex / 15 edge labels
+# (P:1015-1016); the split below is Datagen-like and assumed.
+LDBC_SF10_COUNTS = {"Person": 65_000, "Forum": 600_000, "Post": 7_000_000, "Tag": 16_080, "TagClass": 71,
+                    "City": 1_343, "Country": 111, "Continent": 6, "University": 6_380, "Company": 1_575,
+                    "Filler": 9_434}
+LDBC_SF10_V, LDBC_SF10_E = 35_500_000, 219_400_000
+
+
+def _zipf_pick(rng, n, size, a=0.5):
+    """Indices in [0, n) with P(i) ~ (i+1)^-a (Chung-Lu style weights)."""
+    w = (np.arange(1, n + 1, dtype=np.float64)) ** (-a)
+    c = np.cumsum(w)
+    c /= c[-1]
+    return np.minimum(np.searchsorted(c, rng.random(size)), n - 1).astype(np.int64)
+
+
+def ldbc_graph(scale: float = 1.0, seed: int = 10, sports_frac: float = 0.005) -> Graph:
+    """LDBC-SNB-shaped graph; scale=1.0 is SF10 size (35.5 M vertices,
+    219.4 M edges).  Vertex ids are label-contiguous in LDBC_VERTEX_LABELS
+    order (Post and Comment adjacent = the message range).  Edges:
+      knows      2 M undirected pairs x scale among persons, Zipf(0.5) weights,
+                 80 % inside one of 100 contiguous communities, stored both ways;
+      replyOf    one per comment: a random Post (p = 0.45) else an earlier
+                 comment within 4096 positions (a forest);
+      hasCreator one per message (Zipf person); hasTag one per message (+1 for
+                 15 %), tag 0 = "Sports" with prob sports_frac, else Zipf;
+      containerOf one per post; isLocatedIn one per person and message;
+      hasMember/hasModerator/hasInterest/studyAt/workAt/isPartOf/isSubclassOf/
+      hasType as filler; likes = person -> message, the remainder up to
+      219.4 M x scale edges."""
+    rng = np.random.default_rng(seed)
+    cnt = {k: max(1, int(round(v * scale))) for k, v in LDBC_SF10_COUNTS.items()}
+    for k in ["Tag", "TagClass", "City", "Country", "Continent"]:
+        cnt[k] = max(cnt[k], min(LDBC_SF10_COUNTS[k], 8))
+    nv_target = max(int(round(LDBC_SF10_V * scale)), sum(cnt.values()) + 10)
+    cnt["Comment"] = nv_target - sum(cnt.values())
+    base, off = {}, 0
+    for k in LDBC_VERTEX_LABELS:
+        base[k] = off
+        off += cnt[k]
+    nv = off
+    E = {k: i for i, k in enumerate(LDBC_EDGE_LABELS)}
+    S, D, L = [], [], []
+
+    def add(u, w, lab):
+        S.append(np.asarray(u, dtype=np.uint32))
+        D.append(np.asarray(w, dtype=np.uint32))
+        L.append(np.full(len(u), E[lab], dtype=np.uint16))
+
+    P, F, Po, C, T = cnt["Person"], cnt["Forum"], cnt["Post"], cnt["Comment"], cnt["Tag"]
+    # knows
+    npairs = max(1, int(2_000_000 * scale))
+    u = _zipf_pick(rng, P, npairs)
+    ncomm = 100
+    csize = max(1, P // ncomm)
+    intra = rng.random(npairs) < 0.8
+    comm0 = (u // csize) * csize
+    v_in = comm0 + (csize * rng.random(npairs) ** 2).astype(np.int64)
+    v_in = np.minimum(v_in, P - 1)
+    v_out = _zipf_pick(rng, P, npairs)
+    v = np.where(intra, v_in, v_out)
+    keep = u != v
+    u, v = u[keep] + base["Person"], v[keep] + base["Person"]
+    add(np.concatenate([u, v]), np.concatenate([v, u]), "knows")
+    # replyOf: comment i -> post or earlier comment
+    i = np.arange(C, dtype=np.int64)
+    to_post = (rng.random(C) < 0.45) | (i == 0)
+    back = 1 + (rng.random(C) * np.minimum(np.maximum(i, 1), 4096)).astype(np.int64)
+    parent_c = np.maximum(i - back, 0)
+    parent = np.where(to_post, base["Post"] + rng.integers(0, Po, C), base["Comment"] + parent_c)
+    add(base["Comment"] + i, parent, "replyOf")
+    nmsg = Po + C
+    msg = base["Post"] + np.arange(nmsg, dtype=np.int64)
+    add(msg, base["Person"] + _zipf_pick(rng, P, nmsg), "hasCreator")
+    first = np.where(rng.random(nmsg) < sports_frac, 0, 1 + _zipf_pick(rng, max(1, T - 1), nmsg) % max(1, T - 1))
+    first = np.minimum(first, T - 1)
+    second_m = msg[rng.random(nmsg) < 0.15]
+    add(np.concatenate([msg, second_m]),
+        base["Tag"] + np.concatenate([first, 1 + _zipf_pick(rng, max(1, T - 1), second_m.size) % max(1, T - 1)]),
+        "hasTag")
+    add(base["Forum"] + rng.integers(0, F, Po), base["Post"] + np.arange(Po), "containerOf")
+    ppl = base["Person"] + np.arange(P)
+    add(np.concatenate([ppl, msg]),
+        np.concatenate([base["City"] + rng.integers(0, cnt["City"], P),
+                        base["Country"] + rng.integers(0, cnt["Country"], nmsg)]), "isLocatedIn")
+    nmem = max(1, int(10_000_000 * scale))
+    add(base["Forum"] + rng.integers(0, F, nmem), base["Person"] + _zipf_pick(rng, P, nmem), "hasMember")
+    add(base["Forum"] + np.arange(F), base["Person"] + _zipf_pick(rng, P, F), "hasModerator")
+    nint = P * 10
+    add(base["Person"] + rng.integers(0, P, nint), base["Tag"] + _zipf_pick(rng, T, nint), "hasInterest")
+    add(ppl, base["University"] + rng.integers(0, cnt["University"], P), "studyAt")
+    add(ppl, base["Company"] + rng.integers(0, cnt["Company"], P), "workAt")
+    add(np.concatenate([base["City"] + np.arange(cnt["City"]), base["Country"] + np.arange(cnt["Country"])]),
+        np.concatenate([base["Country"] + rng.integers(0, cnt["Country"], cnt["City"]),
+                        base["Continent"] + rng.integers(0, cnt["Continent"], cnt["Country"])]), "isPartOf")
+    tc = base["TagClass"] + np.arange(1, cnt["TagClass"])
+    add(tc, base["TagClass"] + rng.integers(0, np.maximum(1, tc - base["TagClass"])), "isSubclassOf")
+    add(base["Tag"] + np.arange(T), base["TagClass"] + rng.integers(0, cnt["TagClass"], T), "hasType")
+    fixed = sum(x.size for x in S)
+    nlikes = max(0, int(round(LDBC_SF10_E * scale)) - fixed)
+    add(base["Person"] + _zipf_pick(rng, P, nlikes), base["Post"] + rng.integers(0, nmsg, nlikes), "likes")
+    src = np.concatenate(S)
+    dst = np.concatenate(D)
+    lab = np.concatenate(L)
+    vlab = np.zeros(nv, dtype=np.uint16)
+    for k, name in enumerate(LDBC_VERTEX_LABELS):
+        vlab[base[name]:base[name] + cnt[name]] = k
+    g = _mk(nv, src, dst, lab, LDBC_EDGE_LABELS, vlab, LDBC_VERTEX_LABELS, name="ldbc", scale=scale, seed=seed)
+    g.meta.update({"base": base, "count": cnt, "reply_parent": parent, "sports": base["Tag"]})
+    return g

@@ -239,3 +239,52 @@ def test_cfg2_full_size_sampled():
         want = np.stack([op["src"], op["dst"]], 1).astype(np.uint32)
         want = want[np.lexsort((want[:, 1], want[:, 0]))]
         assert_pairs_equal(rp.rows(), want, rx)
+
+
+def _reply_depths(g):
+    base, cnt = g.meta["base"], g.meta["count"]
+    parent = g.meta["reply_parent"]
+    C = cnt["Comment"]
+    depth = np.zeros(C, np.int64)
+    pc = parent - base["Comment"]
+    is_c = (parent >= base["Comment"]) & (parent < base["Comment"] + C)
+    for i in range(C):
+        depth[i] = 1 + (depth[pc[i]] if is_c[i] else 0)
+    return depth
+
+
+@pytest.mark.parametrize("B", [0, 1024, 4096])
+def test_ldbc_closed_forms(B):
+    """cfg3 shapes: replyOf* on the reply forest = |V| + sum of comment depths
+    (per source: its ancestor chain + itself); knows+ on symmetric knows =
+    component size per person (SURVEY §8(c) closed forms).  Small batches
+    exercise the touched-set clearing / sparse counting paths."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import connected_components
+    g = synth.ldbc_graph(0.002)
+    G = R.rpq_graph_load(g)
+    base, cnt = g.meta["base"], g.meta["count"]
+    depth = _reply_depths(g)
+    a = R.rpq_compile(G, "replyOf*")
+    r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT, batch_sources=B)
+    assert r.count == g.num_vertices + int(depth.sum())
+    r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_PER_SOURCE, batch_sources=B)
+    s, c = r.source_counts()
+    full = np.ones(g.num_vertices, np.uint64)            # epsilon pair of every vertex (R1)
+    full[base["Comment"]:base["Comment"] + cnt["Comment"]] += depth.astype(np.uint64)
+    assert np.array_equal(s, np.arange(g.num_vertices)) and np.array_equal(c, full)
+    P = cnt["Person"]
+    m = g.label == 0
+    A = sp.csr_matrix((np.ones(int(m.sum())), (g.src[m] - base["Person"], g.dst[m] - base["Person"])), shape=(P, P))
+    _, comp = connected_components(A, directed=False)
+    sizes = np.bincount(comp)
+    per = np.where(sizes[comp] >= 2, sizes[comp], 0).astype(np.uint64)
+    k = R.rpq_compile(G, "knows+")
+    r = R.rpq_eval_allpairs(G, k, mode=R.RPQ_PER_SOURCE, batch_sources=min(B, 256) if B else 0)
+    s, c = r.source_counts()
+    want = np.zeros(g.num_vertices, np.uint64)
+    want[base["Person"]:base["Person"] + P] = per
+    got = np.zeros(g.num_vertices, np.uint64)
+    got[s] = c
+    assert np.array_equal(got, want)
+    assert R.rpq_eval_allpairs(G, k, mode=R.RPQ_COUNT, batch_sources=B).count == int(per.sum())
