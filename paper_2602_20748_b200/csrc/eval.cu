@@ -13,23 +13,26 @@
 //
 // B200 design (DESIGN.md has the full rationale and the roofline):
 //   * One bit per source.  A batch of B sources is a column block of
-//     nw = ceil(B/64) 64-bit words.  Three state arrays Vis, F (frontier),
-//     N (next frontier), row-major: word[row * nw + w], one row per
-//     (state q, vertex v in range_q); range_q is the hull of the destination
-//     ranges of the labels entering q (plus the batch's sources for q0), so
-//     states that only live on a label-contiguous vertex block only pay for it.
-//   * A work item is (q, v, chunk) where a chunk is CW consecutive words of
-//     the row; a group of CW lanes expands it: every lane owns one word, the
-//     group walks the per-label CSR rows of v once and each lane updates its
-//     word of the target row (coalesced CW*8-byte segments).
-//   * Discovery is fused: old = atomicOr(Vis[t], f & ~Vis[t]); the truly new
-//     bits go to N[t] with a second atomicOr.  Vis is therefore exact at the
-//     end of every level and no separate "advance" pass exists.  A (row,
-//     chunk) item whose N chunk becomes non-zero is appended once to the next
-//     worklist (activity bitmap, test-before-atomic, warp-aggregated append).
-//   * F words are cleared as they are read, so F and N swap roles each level.
+//     nw = ceil(B/64) 64-bit words.  Two state arrays, row-major
+//     word[row * nw + w], one row per (state q, vertex v in range_q):
+//     Vis (every reached bit) and Done (bits already expanded).  range_q is
+//     the hull of the destination ranges of the labels entering q (plus the
+//     batch's sources for q0; q0 gets no rows when nothing enters it).
+//   * A level is one k_level launch inside a device-driven loop (a CUDA graph
+//     with a conditional WHILE node).  A warp owns one active (row, 32-chunk
+//     block): it advances up to 8 chunks at once (f = Vis & ~Done; Done |= f,
+//     the row's single owner writes Done) and walks the row's per-label CSR
+//     once for all of them, keeping 8 visited-word loads in flight per lane.
+//   * Discovery: m = f & ~Vis[t]; Vis[t] |= m with red.or (no return value,
+//     and the same sector the test just loaded, so it hits L2); the target's
+//     chunk is marked in the next level's activity bitmaps (X per row word,
+//     XB per 32 X words).  k_units lists the active units of each level for
+//     dynamic fetching.  Bits OR-ed into a row before its owner reads Vis in
+//     the same level are expanded early; each bit is still expanded once.
 //   * Rows with more than HUB_EDGES neighbours for a transition are split
-//     into HUB_EDGES segments processed by a second kernel (degree skew).
+//     into HUB_EDGES segments processed by k_level_hub (degree skew).
+//   * Touched (row, chunk) sets let sparse batches clear and count only what
+//     they touched instead of dense memsets.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -107,8 +110,8 @@ struct Ctrl {                  // per-level device counters / flags
 //   X word (r, xw) = which 32-word chunks of the row are active;
 //   XB bit (xi / 32) = some X word in [32 (xi/32), +32) is non-zero.
 struct LevelArgs {
-    uint64_t *N;               // next-frontier accumulator (red.or / exch)
-    uint64_t *Vis;             // visited (written only by the row's owner)
+    uint64_t *Vis;             // visited: every reached bit, OR-ed in by red.or
+    uint64_t *Done;            // bits already expanded (written only by the row's owner)
     uint32_t *Xcur, *Xnext;    // chunk-activity bitmaps, one word per (row, xw)
     uint32_t *XBcur, *XBnext;  // block bitmaps: one bit per 32 X words
     uint64_t nxwords;          // rows * nxw
@@ -243,7 +246,10 @@ __global__ void k_clear_touched(const LevelArgs p, uint32_t ntl) {
                 const uint32_t bt = (uint32_t)(__ffs(x) - 1);
                 x &= x - 1;
                 const uint64_t col = (uint64_t)(xw * 32u + bt) * p.cw + lane;
-                if (lane < (int)p.cw && col < p.nw) p.Vis[row * p.nw + col] = 0ull;
+                if (lane < (int)p.cw && col < p.nw) {
+                    p.Vis[row * p.nw + col] = 0ull;
+                    p.Done[row * p.nw + col] = 0ull;
+                }
             }
         }
     }
@@ -300,7 +306,8 @@ __global__ void k_level_end(Ctrl *ctrl, cudaGraphConditionalHandle h) {
 // active chunks of X word xw (chunk positions packed 8 bits each in `bits`).
 // KC chunks x (8 / KC) edges are in flight per step, so every lane keeps 8
 // independent visited-word loads outstanding.
-//   m = f & ~Vis[t];  N[t] |= m (red);  X/XB activity of t (test, red).
+//   m = f & ~Vis[t];  Vis[t] |= m (red, same sector as the test load, so it
+//   hits L2);  X/XB activity of t (red).
 template <int KC, bool STATS>
 __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S, uint32_t q2,
                                              const uint32_t *__restrict__ nbr, uint32_t beg, uint32_t end,
@@ -337,7 +344,7 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
                 for (int k = 0; k < KC; ++k) {
                     const uint64_t m = f[k] & ~vis[e][k];
                     if (m) {
-                        red_or64(p.N + rb + ckk[k], m);
+                        red_or64(p.Vis + rb + ckk[k], m);
                         if (STATS) st[S_N_RED]++;
                     }
                     if (__ballot_sync(0xffffffffu, m != 0)) newmask |= 1u << ((bits >> (8 * k)) & 0xffu);
@@ -387,7 +394,7 @@ __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const
 
 // Main level kernel: a warp owns one active X word = one row and up to 32 of
 // its chunks; groups of KGRP active chunks are advanced (N -> Vis, fused:
-// f = exch(N, 0) & ~Vis; Vis |= f) and then expanded along every automaton
+// f = Vis & ~Done; Done |= f) and then expanded along every automaton
 // transition of the row's state.  Work units (32 X words = one XB bit) are
 // interleaved over warps.
 template <bool STATS>
@@ -436,9 +443,10 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                 oend = __ldg(off + v + 1);
             }
             while (x) {
-                // take up to KGRP active chunks; advance N -> f (fused):
-                // all visited loads and N exchanges are issued together
-                uint64_t f[KGRP], vv[KGRP];
+                // take up to KGRP active chunks and advance them (fused):
+                // f = Vis & ~Done (bits reached but not yet expanded),
+                // Done |= f; all loads of the group are issued together
+                uint64_t f[KGRP], dd[KGRP];
                 uint64_t bits = 0;
                 int nk = 0;
 #pragma unroll
@@ -449,20 +457,15 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                     nk += has;
                     bits |= (uint64_t)bt << (8 * k);
                     const bool ok = has && lane_ok && xw * 32u * p.cw + bt * p.cw + lane < p.nw;
-                    vv[k] = ok ? ld_cg(p.Vis + rb + bt * p.cw) : ~0ull;
-                    f[k] = ok ? 1ull : 0ull;
+                    f[k] = ok ? ld_cg(p.Vis + rb + bt * p.cw) : 0ull;
+                    dd[k] = ok ? p.Done[rb + bt * p.cw] : ~0ull;
                 }
 #pragma unroll
                 for (int k = 0; k < KGRP; ++k) {
                     const uint32_t bt = (uint32_t)(bits >> (8 * k)) & 0xffu;
-                    if (f[k]) f[k] = atomicExch((unsigned long long *)(p.N + rb + bt * p.cw), 0ull);
-                }
-#pragma unroll
-                for (int k = 0; k < KGRP; ++k) {
-                    const uint32_t bt = (uint32_t)(bits >> (8 * k)) & 0xffu;
-                    f[k] &= ~vv[k];
+                    f[k] &= ~dd[k];
                     if (f[k]) {
-                        p.Vis[rb + bt * p.cw] = vv[k] | f[k];
+                        p.Done[rb + bt * p.cw] = dd[k] | f[k];
                         if (STATS) st[S_WORD_ITEMS]++;
                     }
                 }
@@ -553,14 +556,14 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto
 // would only ever hold the seeds) nothing is written here: k_seed_expand
 // expands the seeds directly and q0 gets no rows at all.
 __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const uint32_t *__restrict__ pidx,
-                       uint64_t b0, uint32_t nb, uint64_t *N, uint32_t *X, uint32_t *XB, uint32_t nw, uint32_t nxw,
+                       uint64_t b0, uint32_t nb, uint64_t *Vis, uint32_t *X, uint32_t *XB, uint32_t nw, uint32_t nxw,
                        uint32_t cw, Ctrl *ctrl, int skip_q0) {
     if (!skip_q0)
         for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
             const uint32_t s = cand[pidx[b0 + i]];
             const uint64_t row = S.row_base[0] + (s - S.lo[0]);
             const uint32_t w = i >> 6, c = w / cw;
-            N[row * nw + w] = 1ull << (i & 63);          // rows are distinct: plain stores
+            Vis[row * nw + w] = 1ull << (i & 63);        // rows are distinct: plain stores
             const uint64_t xi = row * nxw + c / 32;
             X[xi] = 1u << (c & 31);
             atomicOr(XB + (xi >> 10), 1u << ((xi >> 5) & 31));
@@ -1065,7 +1068,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     uint64_t B = o.batch_sources;
     if (B == 0) {
         // bytes per 64-source word column
-        const double per_word = 16.0 * R_max + 0.5 * R_max + 64.0 * 8 * 2;   // Vis + N, bitmaps, extraction
+        const double per_word = 16.0 * R_max + 0.5 * R_max + 64.0 * 8 * 2;   // Vis + Done, bitmaps, extraction
         uint64_t nw_max = per_word > 0 ? (uint64_t)(budget / per_word) : 1;
         if (nw_max < 1) nw_max = 1;
         B = std::min<uint64_t>(std::max<uint64_t>(np, 1), nw_max * 64);
@@ -1099,7 +1102,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     const uint64_t nxwords = R_max * nxw;
     const uint64_t xbwords = (nxwords + 1023) / 1024 + 1;
     const uint32_t hitem_cap = 1u << 14, hrec_cap = 1u << 22;
-    uint64_t *Vis = nullptr, *N = nullptr, *hubF = nullptr;
+    uint64_t *Vis = nullptr, *Done = nullptr, *hubF = nullptr;
     uint32_t *X0 = nullptr, *X1 = nullptr, *XB0 = nullptr, *XB1 = nullptr;
     Ctrl *ctrl = (Ctrl *)ws.get(sizeof(Ctrl));
     unsigned long long *d_stats = (unsigned long long *)ws.get(NSTAT * 8 + 8);
@@ -1111,7 +1114,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     HubItem *hitems = nullptr;
     if (nbatches) {
         Vis = (uint64_t *)ws.get(words * 8);
-        N = (uint64_t *)ws.get(words * 8);
+        Done = (uint64_t *)ws.get(words * 8);
         X0 = (uint32_t *)ws.get(nxwords * 4 + 128);
         X1 = (uint32_t *)ws.get(nxwords * 4 + 128);
         XB0 = (uint32_t *)ws.get(xbwords * 4);
@@ -1119,11 +1122,11 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         hitems = (HubItem *)ws.get((uint64_t)hitem_cap * sizeof(HubItem));
         hubF = (uint64_t *)ws.get((uint64_t)hitem_cap * KGRP * 32 * 8);
         hrecs = (HubRec *)ws.get((uint64_t)hrec_cap * sizeof(HubRec));
-        if (!Vis || !N || !X0 || !X1 || !XB0 || !XB1 || !hitems || !hubF || !hrecs)
+        if (!Vis || !Done || !X0 || !X1 || !XB0 || !XB1 || !hitems || !hubF || !hrecs)
             return fail(rpq_fail(RPQ_ENOMEM, "out of device memory for B=%llu sources (%llu state words)",
                                  (unsigned long long)B, (unsigned long long)words));
         RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(N, 0, words * 8, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(Done, 0, words * 8, s));
         RPQ_CUDA_TRY(cudaMemsetAsync(X0, 0, nxwords * 4 + 128, s));
         RPQ_CUDA_TRY(cudaMemsetAsync(X1, 0, nxwords * 4 + 128, s));
         RPQ_CUDA_TRY(cudaMemsetAsync(XB0, 0, xbwords * 4, s));
@@ -1165,7 +1168,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaMemsetAsync(TU, 0, ((nunits + 31) / 32 + 1) * 4, s));
     }
     LevelArgs P0{}, P1{};
-    P0.N = N; P0.Vis = Vis;
+    P0.Vis = Vis; P0.Done = Done;
     P0.Xcur = X0; P0.Xnext = X1; P0.XBcur = XB0; P0.XBnext = XB1;
     P0.nxwords = nxwords;
     P0.ctrl = ctrl; P0.par = 0;
@@ -1242,6 +1245,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         if (b != (uint64_t)o.shard_index) {   // visited words of the previous batch
             if ((uint64_t)prev_touched * 4 > nunits) {
                 RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
+                RPQ_CUDA_TRY(cudaMemsetAsync(Done, 0, words * 8, s));
                 RPQ_CUDA_TRY(cudaMemsetAsync(TX, 0, nxwords * 4 + 128, s));
                 RPQ_CUDA_TRY(cudaMemsetAsync(TU, 0, ((nunits + 31) / 32 + 1) * 4, s));
             } else if (prev_touched) {
@@ -1250,7 +1254,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
             }
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, &S, sizeof(Layout), cudaMemcpyHostToDevice, s));
-        k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, N, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl,
+        k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, Vis, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl,
                                             skip_q0 ? 1 : 0);
         ST.kernel_launches++;
         if (skip_q0) {
@@ -1277,7 +1281,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         }
         PT.mark("levels");
         if (st != RPQ_OK) return fail(st);
-        // N, X and XB are all zero again here (the last level activated
+        // X and XB are all zero again here (the last level activated
         // nothing).  Extraction reads Vis of the final states.
         const uint32_t vlo = fin_hull.empty() ? 0 : fin_hull.lo;
         const uint64_t vn = fin_hull.empty() ? 0 : (uint64_t)fin_hull.hi - fin_hull.lo + 1;
