@@ -5,7 +5,7 @@ CSRC := $(PKG)/csrc
 LIB := $(PKG)/librpq.so
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Iinclude -I$(CSRC) --expt-relaxed-constexpr
-SRCS := $(CSRC)/eval.cu $(CSRC)/graph.cu $(CSRC)/crpq.cu $(CSRC)/capi.cpp $(CSRC)/regex.cpp
+SRCS := $(CSRC)/eval.cu $(CSRC)/graph.cu $(CSRC)/crpq.cu $(CSRC)/capi.cpp $(CSRC)/regex.cpp $(CSRC)/plan.cpp
 OBJS := $(patsubst $(CSRC)/%,build/%.o,$(SRCS))
 
 all: $(LIB) oracle/liboracle.so

@@ -37,6 +37,13 @@ WORKLOADS = {
     # edges, 4 labels, RPQs a*, (a|b)*c, a b* c, all-pairs, 1 GPU
     "cfg2": {"queries": ["a*", "(a|b)*c", "a b* c"],
              "desc": "uniform random labelled graph |V|=100000 |E|=1000000 (distinct), 4 labels, seed 2"},
+    # configs[2]: LDBC-SNB-shaped SF10-size social graph, replyOf* and knows+
+    "cfg3": {"queries": ["replyOf*", "knows+"],
+             "desc": "LDBC-SNB-shaped synthetic graph, SF10 size (35.5M vertices, 219.4M edges), seed 10"},
+    # configs[4]: RMAT scale 24, 8 labels, (a|b)*c*; one GPU evaluates the
+    # batches of shard 0 of --sample-shards (stated in config.sample)
+    "cfg5": {"queries": ["(a|b)*c*"],
+             "desc": "R-MAT scale 24 (16.8M vertices, 2^28 edge samples), Graph500 A,B,C,D, 8 labels, seed 24"},
 }
 
 
@@ -44,6 +51,10 @@ def make_graph(name):
     import synth
     if name == "cfg2":
         return synth.uniform_graph(100_000, 1_000_000, 4, seed=2)
+    if name == "cfg3":
+        return synth.ldbc_graph(1.0, seed=10)
+    if name == "cfg5":
+        return synth.rmat_graph(24, seed=24)
     raise ValueError(name)
 
 
@@ -144,14 +155,21 @@ def run_ours(args):
     queries = wl["queries"]
 
     # batch width: one batch per rank for N > 1 (round-robin sharding)
+    # the job's batches are shards 0..world-1 of `sample` x world shards; a
+    # sample > 1 (cfg5 on one GPU) evaluates only that fraction of the batches
+    sample = max(1, args.sample_shards)
+    nshard = world * sample
     bsz = {}
     for rx in queries:
         a = R.rpq_compile(G, rx)
-        P = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT, stream=sp).stats()["productive_sources"]
+        st0 = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT, stream=sp, shard_index=0,
+                                  shard_count=max(1, nshard)).stats()
+        P, auto_b = st0["productive_sources"], st0["batch_sources"]
         if args.batch:
             bsz[rx] = args.batch
-        elif world > 1:
-            bsz[rx] = int(-(-P // world) + 63) // 64 * 64
+        elif world > 1 or sample > 1:
+            per = int(-(-P // nshard) + 63) // 64 * 64
+            bsz[rx] = max(64, min(auto_b, per))
         else:
             bsz[rx] = 0
     # per-rank probe with the in-kernel counters (RPQ_STATS): PE and the
@@ -160,7 +178,7 @@ def run_ours(args):
     for rx in queries:
         a = R.rpq_compile(G, rx)
         r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=sp, batch_sources=bsz[rx],
-                                shard_index=rank, shard_count=world)
+                                shard_index=rank, shard_count=nshard)
         probe[rx] = r.stats()
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")   # > 126 MB L2
@@ -170,7 +188,7 @@ def run_ours(args):
         for rx in queries:
             a = R.rpq_compile(G, rx)
             r = R.rpq_eval_allpairs(G, a, mode=mode, stream=sp, batch_sources=bsz[rx],
-                                    shard_index=rank, shard_count=world)
+                                    shard_index=rank, shard_count=nshard)
             st = r.stats()
             tot["count"] += r.count
             tot["launches"] += st["kernel_launches"]
@@ -239,7 +257,7 @@ def run_ours(args):
         for rx in queries:
             a = R.rpq_compile(G2, rx)
             r = R.rpq_eval_allpairs(G2, a, mode=R.RPQ_COUNT, stream=sp, batch_sources=bsz[rx],
-                                    shard_index=rank, shard_count=world)
+                                    shard_index=rank, shard_count=nshard)
             _ = r.count                                  # device -> host result
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) * 1e3
@@ -280,7 +298,9 @@ def run_ours(args):
                    "pe_per_step": pe_per_step, "pairs_per_step": count_total / args.steps,
                    "batch_sources": {rx: probe[rx]["batch_sources"] if not bsz[rx] else bsz[rx] for rx in queries},
                    "parallelism": f"source-batch shards x{world}",
-                   "l2": "flushed between timed steps (256 MiB write)"},
+                   "l2": "flushed between timed steps (256 MiB write)",
+                   "sample": "all batches" if sample == 1 else
+                             f"batches of shards 0..{world - 1} of {nshard} (1/{sample} of the all-pairs query)"},
         "roofline": {"bound": "hbm", "kernel": "k_level (level loop: k_units + k_level + k_level_hub)",
                      "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s",
@@ -369,12 +389,16 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS))
     ap.add_argument("--batch", type=int, default=0, help="source batch width B (0 = auto)")
+    ap.add_argument("--sample-shards", type=int, default=0,
+                    help="evaluate 1/S of the batches (default: 16 for cfg5 on one GPU, else 1)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.sample_shards == 0:
+        args.sample_shards = 16 if (args.workload == "cfg5" and args.gpus == 1) else 1
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -220,6 +220,15 @@ rpq_status rpq_result_source_counts(const rpq_result *r, uint32_t *srcs, uint64_
 rpq_status rpq_result_stats(const rpq_result *r, rpq_stats *s);
 void rpq_result_free(rpq_result *r);
 
+/* Host-only: the shard that owns each candidate source under the batch plan
+ * of rpq_eval_* (productive candidates pidx[0..np) ascending, batches of
+ * batch_sources consecutive productive sources, batch b -> shard
+ * b % shard_count; non-productive candidates belong to the batch before them,
+ * and all to shard 0 when np == 0).  owner: host [nsrc].  Used to test and
+ * reason about multi-GPU sharding without a GPU. */
+rpq_status rpq_shard_plan(const uint32_t *pidx, uint64_t np, uint64_t nsrc, uint64_t batch_sources,
+                          uint32_t shard_count, uint32_t *owner);
+
 const char *rpq_last_error(void);
 /* number of usable CUDA devices (0 on a machine without a GPU) */
 rpq_status rpq_device_count(int *n);

@@ -108,7 +108,7 @@ EXPORTED = [
     "rpq_nfa_accepts", "rpq_eval_allpairs", "rpq_eval_single_source", "rpq_eval_sources",
     "crpq_eval", "rpq_result_count", "rpq_result_device_view", "rpq_result_copy_host",
     "rpq_result_source_counts", "rpq_result_stats", "rpq_result_free", "rpq_last_error",
-    "rpq_device_count", "rpq_version",
+    "rpq_device_count", "rpq_version", "rpq_shard_plan",
 ]
 
 _c = {}
@@ -140,6 +140,8 @@ _c["rpq_result_free"] = _proto("rpq_result_free", None, [_vp])
 _c["rpq_last_error"] = _proto("rpq_last_error", ctypes.c_char_p, [])
 _c["rpq_device_count"] = _proto("rpq_device_count", _st, [_P(ctypes.c_int)])
 _c["rpq_version"] = _proto("rpq_version", ctypes.c_char_p, [])
+_c["rpq_shard_plan"] = _proto("rpq_shard_plan", _st, [c_u32p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                                      ctypes.c_uint32, c_u32p])
 
 
 def _check(st: int, offset: int = 0):
@@ -271,6 +273,15 @@ def rpq_device_count() -> int:
 
 def rpq_version() -> str:
     return _c["rpq_version"]().decode()
+
+
+def rpq_shard_plan(productive_idx, num_candidates: int, batch_sources: int, shard_count: int) -> np.ndarray:
+    """Owner shard of every candidate source (host-only, see include/rpq.h)."""
+    p = _arr(productive_idx if len(productive_idx) else [0], np.uint32)
+    owner = np.zeros(max(1, num_candidates), np.uint32)
+    _check(_c["rpq_shard_plan"](_ptr(p, ctypes.c_uint32), len(productive_idx), num_candidates, batch_sources,
+                                shard_count, _ptr(owner, ctypes.c_uint32)))
+    return owner[:num_candidates]
 
 
 def rpq_last_error() -> str:

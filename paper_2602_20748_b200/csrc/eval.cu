@@ -1152,7 +1152,9 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     uint64_t total = 0;
     // candidate-index interval owned by batch b (non-productive candidates in
     // it contribute their epsilon pair); one virtual batch when P is empty
-    auto jstart = [&](uint64_t b) -> uint64_t { return b == 0 ? 0 : (b < nbatches ? bfirst[b] : nsrc); };
+    std::vector<uint64_t> js;   // batch b owns candidates [js[b], js[b+1]) (plan.cpp)
+    batch_plan(bfirst.data(), nbatches, nsrc, js);
+    auto jstart = [&](uint64_t b) -> uint64_t { return js[b]; };
     const uint64_t nb_eff = std::max<uint64_t>(nbatches, 1);
 
     // ---- level loop setup: parity-0/1 argument sets and the device graph ----

@@ -69,6 +69,10 @@ void rpq_result_release(rpq_result *r);
 rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint32_t *d_sources,
                                uint64_t nsrc, const rpq_eval_opts *opts, rpq_result **out);
 
+// ---- batch plan (plan.cpp) -----------------------------------------------
+// jstart[b] = first candidate index owned by batch b (nb_eff + 1 entries)
+void batch_plan(const uint32_t *bfirst, uint64_t nbatches, uint64_t nsrc, std::vector<uint64_t> &jstart);
+
 // ---- compile (regex.cpp) -------------------------------------------------
 rpq_status compile_regex(const std::vector<std::string> &vocab, const char *regex, uint32_t flags,
                          rpq_nfa **out, size_t *err_offset);
