@@ -61,6 +61,22 @@ void *dev_alloc(size_t bytes, void *stream) {
     return p;
 }
 
+// Bytes an evaluation can still allocate: free device memory plus what the
+// stream-ordered pool has reserved but is not using (it keeps freed blocks).
+uint64_t dev_available() {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); return 0; }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    uint64_t reserved = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    return (uint64_t)free_b + (reserved > used ? reserved - used : 0);
+}
+
 void dev_free(void *p, void *stream) {
     if (p) cudaFreeAsync(p, (cudaStream_t)stream);
 }

@@ -224,7 +224,9 @@ __global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
 // A warp per touched unit (32 X words): zero the visited words of every
 // chunk the batch touched, and the touched bitmaps, so the next batch starts
 // clean without a dense memset of the whole state.
-__global__ void k_clear_touched(const LevelArgs p, uint32_t ntl) {
+__global__ void k_clear_touched(const LevelArgs p, uint64_t nunits) {
+    const uint32_t ntl = p.ctrl->ntouched;
+    if ((uint64_t)ntl * 4 > nunits) return;      // dense: k_clear_dense does it
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -258,8 +260,10 @@ __global__ void k_clear_touched(const LevelArgs p, uint32_t ntl) {
 // COUNT over the touched chunks only: bits of Vis[q][v][w] for final q that
 // are not already set in a lower-numbered final state's row of v (the OR over
 // final states, counted once).
-__global__ void k_count_touched(const DevAuto A, const Layout S, const LevelArgs p, uint32_t ntl,
+__global__ void k_count_touched(const DevAuto A, const Layout S, const LevelArgs p, uint64_t nunits,
                                 unsigned long long *total) {
+    const uint32_t ntl = p.ctrl->ntouched;
+    if ((uint64_t)ntl * 4 > nunits) return;      // dense batch: k_count_total counts
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -626,6 +630,29 @@ __global__ void k_productive(const DevAuto A, const uint32_t *__restrict__ cand,
     }
 }
 
+// per batch: first/last productive candidate index and their vertex ids
+__global__ void k_batch_bounds(const uint32_t *pidx, const uint32_t *cand, uint64_t np, uint64_t B, uint64_t nbatches,
+                               uint32_t *out) {
+    for (uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; b < nbatches; b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t f = pidx[b * B], l = pidx[min(np, (b + 1) * B) - 1];
+        out[4 * b + 0] = f;
+        out[4 * b + 1] = l;
+        out[4 * b + 2] = cand[f];
+        out[4 * b + 3] = cand[l];
+    }
+}
+
+// Dense clear of the batch state, only when the finished batch touched a
+// large fraction of it (device-side decision: no host round trip).
+__global__ void k_clear_dense(uint64_t *Vis, uint64_t *Done, uint64_t words, uint32_t *TX, uint64_t nxwords,
+                              uint32_t *TU, uint64_t ntu, const Ctrl *ctrl, uint64_t nunits) {
+    if ((uint64_t)ctrl->ntouched * 4 <= nunits) return;
+    const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = i0; i < words; i += st) { Vis[i] = 0; Done[i] = 0; }
+    for (uint64_t i = i0; i < nxwords; i += st) TX[i] = 0;
+    for (uint64_t i = i0; i < ntu; i += st) TU[i] = 0;
+}
+
 __global__ void k_iota(uint32_t *x, uint64_t n) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
         x[j] = (uint32_t)j;
@@ -649,7 +676,8 @@ __device__ __forceinline__ uint64_t ans_word(const DevAuto &A, const Layout &S, 
 
 // COUNT: total popcount of Ans over the hull [vlo, vlo + vn) x [0, nw).
 __global__ void k_count_total(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
-                              uint32_t nw, unsigned long long *total) {
+                              uint32_t nw, unsigned long long *total, const Ctrl *ctrl, uint64_t nunits) {
+    if (ctrl && (uint64_t)ctrl->ntouched * 4 <= nunits) return;   // sparse batch: k_count_touched counts
     unsigned long long acc = 0;
     const uint64_t n = vn * nw;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -1062,9 +1090,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         if (q == 0 && np && !skip_q0) r = hull(r, Range{p_first, p_last});
         R_max += r.empty() ? 0 : (uint64_t)r.hi - r.lo + 1;
     }
-    size_t free_b = 0, total_b = 0;
-    RPQ_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-    uint64_t budget = o.hbm_budget_bytes ? o.hbm_budget_bytes : (uint64_t)(free_b * 0.9);
+    uint64_t budget = o.hbm_budget_bytes ? o.hbm_budget_bytes : (uint64_t)(dev_available() * 0.9);
     uint64_t B = o.batch_sources;
     if (B == 0) {
         // bytes per 64-source word column
@@ -1086,13 +1112,21 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     ST.chunk_words = CW;
 
     // batch boundaries: first/last productive candidate index of each batch
-    std::vector<uint32_t> bfirst(nbatches), blast(nbatches);
-    for (uint64_t b = 0; b < nbatches; ++b) {
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&bfirst[b], pidx + b * B, 4, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&blast[b], pidx + std::min<uint64_t>(np, (b + 1) * B) - 1, 4,
-                                     cudaMemcpyDeviceToHost, s));
+    // and their vertex ids (one kernel + one copy for all batches)
+    std::vector<uint32_t> bfirst(nbatches), blast(nbatches), sfirst(nbatches), slast(nbatches);
+    if (nbatches) {
+        uint32_t *d_bounds = (uint32_t *)ws.get(nbatches * 16);
+        if (!d_bounds) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+        k_batch_bounds<<<grid_for(nbatches), 256, 0, s>>>(pidx, cand, np, B, nbatches, d_bounds);
+        ST.kernel_launches++;
+        std::vector<uint32_t> hb(nbatches * 4);
+        RPQ_CUDA_TRY(cudaMemcpyAsync(hb.data(), d_bounds, nbatches * 16, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        for (uint64_t b = 0; b < nbatches; ++b) {
+            bfirst[b] = hb[4 * b]; blast[b] = hb[4 * b + 1];
+            sfirst[b] = hb[4 * b + 2]; slast[b] = hb[4 * b + 3];
+        }
     }
-    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
 
     PT.mark("batch plan");
     // ---- workspace ----------------------------------------------------------
@@ -1198,7 +1232,38 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     }
     PT.mark("level graph");
 
-    uint32_t prev_touched = 0;   // touched units of the previous batch of this shard
+    // layouts of this shard's batches, computed up front and copied once
+    std::vector<Layout> lay_h;
+    std::vector<Range> lay_fin;
+    for (uint64_t b = o.shard_index; b < nbatches; b += shard_count) {
+        Layout S{};
+        uint64_t rows = 0;
+        Range fin_hull{1, 0};
+        for (uint32_t q = 0; q < a->nq; ++q) {
+            Range r = in_range[q];
+            if (q == 0 && !skip_q0) r = hull(r, Range{sfirst[b], slast[b]});
+            S.row_base[q] = rows;
+            S.lo[q] = r.empty() ? 0 : r.lo;
+            S.len[q] = r.empty() ? 0 : r.hi - r.lo + 1;
+            rows += S.len[q];
+            if ((a->final_mask >> q) & 1) fin_hull = hull(fin_hull, r);
+        }
+        lay_h.push_back(S);
+        lay_fin.push_back(fin_hull);
+    }
+    Layout *d_layouts = (Layout *)ws.get(std::max<size_t>(lay_h.size(), 1) * sizeof(Layout));
+    if (!d_layouts) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+    if (!lay_h.empty()) {
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_layouts, lay_h.data(), lay_h.size() * sizeof(Layout), cudaMemcpyHostToDevice, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_total, 0, 8, s));
+    size_t lay_i = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+    struct TevGuard {
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *v;
+        ~TevGuard() { for (auto &e : *v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); } }
+    } tevg{&tev};
     for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count) {
         const uint64_t jlo = jstart(b), jhi = (b + 1 < nb_eff) ? jstart(b + 1) : nsrc;
         ST.batches++;
@@ -1227,35 +1292,16 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         }
         const uint64_t b0 = b * B;
         const uint32_t nb = (uint32_t)std::min<uint64_t>(B, np - b0);
-        // layout for this batch
-        uint32_t s_first = 0, s_last = 0;
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&s_first, cand + bfirst[b], 4, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&s_last, cand + blast[b], 4, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        Layout S{};
-        uint64_t rows = 0;
-        Range fin_hull{1, 0};
-        for (uint32_t q = 0; q < a->nq; ++q) {
-            Range r = in_range[q];
-            if (q == 0 && !skip_q0) r = hull(r, Range{s_first, s_last});
-            S.row_base[q] = rows;
-            S.lo[q] = r.empty() ? 0 : r.lo;
-            S.len[q] = r.empty() ? 0 : r.hi - r.lo + 1;
-            rows += S.len[q];
-            if ((a->final_mask >> q) & 1) fin_hull = hull(fin_hull, r);
+        const Layout &S = lay_h[lay_i];
+        const Range fin_hull = lay_fin[lay_i];
+        if (lay_i > 0) {   // clear what the previous batch of this shard touched
+            k_clear_touched<<<148 * 8, 256, 0, s>>>(P0, nunits);
+            k_clear_dense<<<148 * 8, 256, 0, s>>>(Vis, Done, words, TX, nxwords + 32, TU, (nunits + 31) / 32 + 1,
+                                                  ctrl, nunits);
+            ST.kernel_launches += 2;
         }
-        if (b != (uint64_t)o.shard_index) {   // visited words of the previous batch
-            if ((uint64_t)prev_touched * 4 > nunits) {
-                RPQ_CUDA_TRY(cudaMemsetAsync(Vis, 0, words * 8, s));
-                RPQ_CUDA_TRY(cudaMemsetAsync(Done, 0, words * 8, s));
-                RPQ_CUDA_TRY(cudaMemsetAsync(TX, 0, nxwords * 4 + 128, s));
-                RPQ_CUDA_TRY(cudaMemsetAsync(TU, 0, ((nunits + 31) / 32 + 1) * 4, s));
-            } else if (prev_touched) {
-                k_clear_touched<<<grid_for((uint64_t)prev_touched * 32), 256, 0, s>>>(P0, prev_touched);
-                ST.kernel_launches++;
-            }
-        }
-        RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, &S, sizeof(Layout), cudaMemcpyHostToDevice, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, d_layouts + lay_i, sizeof(Layout), cudaMemcpyDeviceToDevice, s));
+        ++lay_i;
         k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, Vis, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl,
                                             skip_q0 ? 1 : 0);
         ST.kernel_launches++;
@@ -1267,20 +1313,19 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         }
         PT.mark("seed");
         rpq_status st = RPQ_OK;
-        if (timeit) cudaEventRecord(evt0, s);
+        if (timeit) {
+            tev.emplace_back();
+            cudaEventCreate(&tev.back().first);
+            cudaEventCreate(&tev.back().second);
+            cudaEventRecord(tev.back().first, s);
+        }
         if (LG.exec) {
             cudaError_t ge = cudaGraphLaunch(LG.exec, s);
             if (ge != cudaSuccess) st = rpq_fail(RPQ_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(ge));
         } else {
             st = run_levels_host(A, d_layout, P0, P1, lgrid, hgrid, xbwords, s, stats, h_cnt, &ST);
         }
-        if (timeit) {
-            cudaEventRecord(evt1, s);
-            cudaEventSynchronize(evt1);
-            float ms = 0;
-            cudaEventElapsedTime(&ms, evt0, evt1);
-            ST.expand_ms += ms;
-        }
+        if (timeit) cudaEventRecord(tev.back().second, s);
         PT.mark("levels");
         if (st != RPQ_OK) return fail(st);
         // X and XB are all zero again here (the last level activated
@@ -1288,24 +1333,14 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         const uint32_t vlo = fin_hull.empty() ? 0 : fin_hull.lo;
         const uint64_t vn = fin_hull.empty() ? 0 : (uint64_t)fin_hull.hi - fin_hull.lo + 1;
         const uint64_t eps_np = eps ? (jhi - jlo) - nb : 0;   // non-productive candidates in the interval
-        RPQ_CUDA_TRY(cudaMemcpyAsync(h_cnt + 4, &ctrl->ntouched, 4, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        prev_touched = h_cnt[4];
-        const bool sparse = (uint64_t)prev_touched * 4 <= nunits;
         if (!want_ps) {
-            RPQ_CUDA_TRY(cudaMemsetAsync(d_total, 0, 8, s));
-            if (sparse && prev_touched) {
-                k_count_touched<<<grid_for((uint64_t)prev_touched * 32), 256, 0, s>>>(A, S, P0, prev_touched,
-                                                                                    d_total);
-                ST.kernel_launches++;
-            } else if (vn) {
-                k_count_total<<<grid_for(vn * nw), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, d_total);
-                ST.kernel_launches++;
-            }
-            unsigned long long t = 0;
-            RPQ_CUDA_TRY(cudaMemcpyAsync(&t, d_total, 8, cudaMemcpyDeviceToHost, s));
-            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-            total += t + eps_np;
+            // COUNT: accumulate on the device (sparse or dense path chosen
+            // there from the touched-unit count); no host round trip
+            k_count_touched<<<148 * 8, 256, 0, s>>>(A, S, P0, nunits, d_total);
+            if (vn) k_count_total<<<grid_for(vn * nw), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, d_total, ctrl,
+                                                                     nunits);
+            ST.kernel_launches += vn ? 2 : 1;
+            total += eps_np;
             continue;
         }
         const uint32_t nseg = (uint32_t)std::max<uint64_t>(1, (vn + TILE_V - 1) / TILE_V);
@@ -1357,6 +1392,18 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaGetLastError());
     }
 
+    if (!want_ps && nbatches) {
+        unsigned long long t = 0;
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&t, d_total, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        total += t;
+    }
+    for (auto &e : tev) {
+        float ms = 0;
+        cudaEventSynchronize(e.second);
+        cudaEventElapsedTime(&ms, e.first, e.second);
+        ST.expand_ms += ms;
+    }
     PT.mark("extraction");
     // ---- result assembly ---------------------------------------------------
     res->count = total;
