@@ -1093,9 +1093,24 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     uint64_t budget = o.hbm_budget_bytes ? o.hbm_budget_bytes : (uint64_t)(dev_available() * 0.9);
     uint64_t B = o.batch_sources;
     if (B == 0) {
-        // bytes per 64-source word column
-        const double per_word = 16.0 * R_max + 0.5 * R_max + 64.0 * 8 * 2;   // Vis + Done, bitmaps, extraction
-        uint64_t nw_max = per_word > 0 ? (uint64_t)(budget / per_word) : 1;
+        // bytes per 64-source word column: Vis + Done, bitmaps, and for
+        // PER_SOURCE / PAIRS the per-(source, 1024-vertex tile) counts; the
+        // materialised pairs are allocated outside the budget, so those modes
+        // keep half of it free
+        double per_word = 16.0 * R_max + 0.5 * R_max + 64.0 * 8 * 2;
+        uint64_t bud = budget;
+        if (want_ps) {
+            uint64_t hullv = 0;
+            for (uint32_t q = 0; q < a->nq; ++q)
+                if ((a->final_mask >> q) & 1) {
+                    Range r = in_range[q];
+                    if (q == 0 && np) r = hull(r, Range{p_first, p_last});
+                    hullv = std::max<uint64_t>(hullv, r.empty() ? 0 : (uint64_t)r.hi - r.lo + 1);
+                }
+            per_word += 64.0 * (4.0 * ((double)hullv / TILE_V + 1) + 24.0);
+            bud /= 2;
+        }
+        uint64_t nw_max = per_word > 0 ? (uint64_t)(bud / per_word) : 1;
         if (nw_max < 1) nw_max = 1;
         B = std::min<uint64_t>(std::max<uint64_t>(np, 1), nw_max * 64);
     }

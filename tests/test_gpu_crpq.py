@@ -73,3 +73,20 @@ def test_crpq_errors(toy):
     with pytest.raises(R.RPQError) as e:      # variable in no atom
         R.crpq_eval(G, [-1, -1, -1], [-1, -1, -1], [(0, nfa, 1)])
     assert e.value.status == R.RPQ_EUNSUPPORTED
+
+
+def test_cfg4_ldbc_crpq_small():
+    """BASELINE cfg4 shape: m -hasTag-> t:Sports, m -hasCreator-> u,
+    m -replyOf*-> p:Post.  Against the oracle's hash join of O1 relations and
+    the closed form (one tuple per Sports-tagged message: one creator, one
+    root post)."""
+    g = synth.ldbc_graph(0.002)
+    G = R.rpq_graph_load(g)
+    sports = g.meta["sports"]
+    vars_ = ["m", "t", "u", "p"]
+    atoms = [("m", "hasTag", "t"), ("m", "hasCreator", "u"), ("m", "replyOf*", "p")]
+    got = rows(R.crpq(G, vars_, atoms, var_label={"p": "Post"}, var_const={"t": sports}))
+    q = oracle.CRPQ(vars_, atoms, var_label={"p": "Post"}, var_const={"t": sports})
+    assert got == oracle.crpq_join(g, q)
+    tagged = set(g.src[(g.label == g.label_names.index("hasTag")) & (g.dst == sports)].tolist())
+    assert len(got) == len(tagged) and {t[0] for t in got} == tagged
