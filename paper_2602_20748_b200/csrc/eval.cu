@@ -316,7 +316,7 @@ template <int KC, bool STATS>
 __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S, uint32_t q2,
                                              const uint32_t *__restrict__ nbr, uint32_t beg, uint32_t end,
                                              const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
-                                             unsigned long long *st, bool &act) {
+                                             unsigned long long *st, bool &act, bool live) {
     constexpr int E = SLOTS / KC;
     const uint32_t tbase = (uint32_t)(S.row_base[q2] - S.lo[q2]);
     const uint32_t colbase = xw * 32u * p.cw + lane;
@@ -351,8 +351,10 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
                         red_or64(p.Vis + rb + ckk[k], m);
                         if (STATS) st[S_N_RED]++;
                     }
-                    if (__ballot_sync(0xffffffffu, m != 0)) newmask |= 1u << ((bits >> (8 * k)) & 0xffu);
+                    if (live && __ballot_sync(0xffffffffu, m != 0)) newmask |= 1u << ((bits >> (8 * k)) & 0xffu);
                 }
+                // a target state without outgoing transitions is never
+                // expanded: its rows only collect result bits, no activity
                 if (lane == 0 && newmask) {
                     // activity of the target row: fire-and-forget ORs (the
                     // words are idempotent; no test load on the critical path)
@@ -389,11 +391,11 @@ template <bool STATS>
 __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const Layout &S, uint32_t q2,
                                                const uint32_t *nbr, uint32_t beg, uint32_t end,
                                                const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
-                                               unsigned long long *st, bool &act) {
-    if (nk > 4) expand_edges<8, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act);
-    else if (nk > 2) expand_edges<4, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act);
-    else if (nk > 1) expand_edges<2, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act);
-    else expand_edges<1, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act);
+                                               unsigned long long *st, bool &act, bool live) {
+    if (nk > 4) expand_edges<8, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+    else if (nk > 2) expand_edges<4, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+    else if (nk > 1) expand_edges<2, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+    else expand_edges<1, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
 }
 
 // Main level kernel: a warp owns one active X word = one row and up to 32 of
@@ -519,7 +521,8 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                                 p.hrecs[r + sg] = HubRec{0u, 0u, 0u, 0u};
                         }
                     }
-                    dispatch_edges<STATS>(nk, p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act);
+                    dispatch_edges<STATS>(nk, p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act,
+                                          A.toff[A.tto[t] + 1] > A.toff[A.tto[t]]);
                 }
             }
         }
@@ -548,7 +551,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto
 #pragma unroll
         for (int k = 0; k < KGRP; ++k) f[k] = p.hubF[((uint64_t)r.hitem * KGRP + k) * 32 + lane];
         dispatch_edges<STATS>((int)h.nk, p, S, A.tto[r.t], A.nbr[A.tslot[r.t]], r.beg, r.end, f, h.bits, h.xw, lane,
-                              st, act);
+                              st, act, A.toff[A.tto[r.t] + 1] > A.toff[A.tto[r.t]]);
     }
     if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
     flush_stats<STATS>(st, p.stats);
@@ -610,7 +613,8 @@ __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layo
             const uint32_t beg = __ldg(A.off[slot] + sv), end = __ldg(A.off[slot] + sv + 1);
             if (STATS && lane == 0) st[S_ITEM_TRANS]++;
             if (end > beg)
-                expand_edges<1, STATS>(p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act);
+                expand_edges<1, STATS>(p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act,
+                                       A.toff[A.tto[t] + 1] > A.toff[A.tto[t]]);
         }
     }
     if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
@@ -1121,6 +1125,13 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     if (CW != 1 && CW != 2 && CW != 4 && CW != 8 && CW != 16 && CW != 32)
         return fail(rpq_fail(RPQ_EINVAL, "chunk_words must be 1,2,4,8,16 or 32"));
     nw = (nw + CW - 1) / CW * CW;
+    {
+        // optional row alignment (RPQ_NW_ALIGN words); measured neutral for
+        // cfg2 at 256 words = 2 KB, so off by default
+        const char *ea = getenv("RPQ_NW_ALIGN");
+        const uint64_t al = ea ? strtoull(ea, nullptr, 10) : 1;
+        if (al > 1 && nw >= al) nw = (nw + al - 1) / al * al;
+    }
     const uint64_t nchunk = nw / CW;
     const uint64_t nbatches = np ? (np + B - 1) / B : 0;
     ST.batch_sources = (uint32_t)B;
