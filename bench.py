@@ -125,11 +125,12 @@ class ClockSampler:
 
 
 def algorithmic_bytes(st):
-    """Bytes the fused level kernel must move:
-    32 B per advanced word (N exch read+write, Vis read+write), 8 B per
-    (row-group, transition) offset pair, 4 B per (row-group, edge) neighbour
-    id, 16 B per (word, edge) operation (visited read + next-frontier OR)."""
-    return (32 * st["word_items"] + 8 * st["item_transitions"] + 4 * st["item_edges"]
+    """Bytes the fused level kernel must move: 24 B per
+    advanced word (Vis read, Done read, Done write), 8 B per (row-group,
+    transition) CSR offset pair, 4 B per (row-group, edge) neighbour id, 16 B
+    per (non-zero frontier word, edge) operation (visited read 8 B + the OR of
+    the new bits into it 8 B -- SURVEY.md §8(d)'s "Vis read + Next RMW")."""
+    return (24 * st["word_items"] + 8 * st["item_transitions"] + 4 * st["item_edges"]
             + 16 * st["word_edge_ops"])
 
 
