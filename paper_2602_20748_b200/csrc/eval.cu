@@ -329,24 +329,29 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
     for (uint32_t j = beg; j < end; j += 32) {
         const uint32_t my = (j + lane < end) ? __ldg(nbr + j + lane) : 0u;
         const int cnt = (int)((end - j) < 32u ? (end - j) : 32u);
-        for (int e0 = 0; e0 < cnt; e0 += E) {
+        // one step: issue all loads of E edges x KC chunks, then the ORs
+        struct Buf {
             uint32_t trow[E];
             uint64_t vis[E][KC];
+        };
+        auto issue = [&](Buf &b, int e0) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 const bool ok = e0 + e < cnt;
-                trow[e] = tbase + __shfl_sync(0xffffffffu, my, (e0 + e) & 31);
-                const uint64_t rb = (uint64_t)trow[e] * p.nw + colbase;
+                b.trow[e] = tbase + __shfl_sync(0xffffffffu, my, (e0 + e) & 31);
+                const uint64_t rb = (uint64_t)b.trow[e] * p.nw + colbase;
 #pragma unroll
-                for (int k = 0; k < KC; ++k) vis[e][k] = (ok && f[k]) ? ld_cg(p.Vis + rb + ckk[k]) : ~0ull;
+                for (int k = 0; k < KC; ++k) b.vis[e][k] = (ok && f[k]) ? ld_cg(p.Vis + rb + ckk[k]) : ~0ull;
             }
+        };
+        auto process = [&](const Buf &b, int e0) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
                 uint32_t newmask = 0;
-                const uint64_t rb = (uint64_t)trow[e] * p.nw + colbase;
+                const uint64_t rb = (uint64_t)b.trow[e] * p.nw + colbase;
 #pragma unroll
                 for (int k = 0; k < KC; ++k) {
-                    const uint64_t m = f[k] & ~vis[e][k];
+                    const uint64_t m = (e0 + e < cnt) ? (f[k] & ~b.vis[e][k]) : 0ull;
                     if (m) {
                         red_or64(p.Vis + rb + ckk[k], m);
                         if (STATS) st[S_N_RED]++;
@@ -358,13 +363,20 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
                 if (lane == 0 && newmask) {
                     // activity of the target row: fire-and-forget ORs (the
                     // words are idempotent; no test load on the critical path)
-                    const uint64_t xi = (uint64_t)trow[e] * p.nxw + xw;
+                    const uint64_t xi = (uint64_t)b.trow[e] * p.nxw + xw;
                     red_or32(p.Xnext + xi, newmask);
                     red_or32(p.XBnext + (xi >> 10), 1u << ((xi >> 5) & 31));
                     act = true;
                     if (STATS) st[S_X_RED]++;
                 }
             }
+        };
+        // (double-buffering the steps was measured slower: more registers,
+        // no gain -- the loop is not bound by the latency of one step)
+        for (int e0 = 0; e0 < cnt; e0 += E) {
+            Buf b;
+            issue(b, e0);
+            process(b, e0);
         }
         if (STATS && nzw) {
             st[S_WORD_EDGE] += (unsigned long long)nzw * cnt;
