@@ -224,9 +224,9 @@ __global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
 // A warp per touched unit (32 X words): zero the visited words of every
 // chunk the batch touched, and the touched bitmaps, so the next batch starts
 // clean without a dense memset of the whole state.
-__global__ void k_clear_touched(const LevelArgs p, uint64_t nunits) {
+__global__ void k_clear_touched(const LevelArgs p, uint64_t nunits, int force_dense) {
     const uint32_t ntl = p.ctrl->ntouched;
-    if ((uint64_t)ntl * 4 > nunits) return;      // dense: k_clear_dense does it
+    if (force_dense || (uint64_t)ntl * 4 > nunits) return;      // dense: k_clear_dense does it
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -261,9 +261,9 @@ __global__ void k_clear_touched(const LevelArgs p, uint64_t nunits) {
 // are not already set in a lower-numbered final state's row of v (the OR over
 // final states, counted once).
 __global__ void k_count_touched(const DevAuto A, const Layout S, const LevelArgs p, uint64_t nunits,
-                                unsigned long long *total) {
+                                unsigned long long *total, int force_dense) {
     const uint32_t ntl = p.ctrl->ntouched;
-    if ((uint64_t)ntl * 4 > nunits) return;      // dense batch: k_count_total counts
+    if (force_dense || (uint64_t)ntl * 4 > nunits) return;      // dense batch: k_count_total counts
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -633,6 +633,137 @@ __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layo
     flush_stats<STATS>(st, p.stats);
 }
 
+// ---- sparse engine ----------------------------------------------------------
+// For queries whose per-source reach is small (replyOf* chains, selective
+// atoms), a warp evaluates one source at a time: the product-graph BFS of
+// P:252-257 with the visited set as an open-addressing hash set of (v, q)
+// keys and the frontier as a FIFO, both in shared memory.  Distinct final
+// targets are counted through marker keys (v, 255) in the same set.  A source
+// whose reach outgrows the warp's capacity is flagged and re-evaluated by the
+// dense bit-parallel engine.
+constexpr int SP_WARPS = 4;
+constexpr int SP_H = 1024;           // hash slots per warp (u64 keys)
+constexpr int SP_Q = 512;            // FIFO capacity per warp
+constexpr int SP_PROBES = 32;
+constexpr uint64_t SP_EMPTY = ~0ull;
+
+__device__ __forceinline__ int sp_insert(uint64_t *tab, uint64_t key) {
+    uint32_t h = (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 54);   // 10 bits
+    for (int pr = 0; pr < SP_PROBES; ++pr) {
+        const uint64_t old = atomicCAS((unsigned long long *)&tab[h], (unsigned long long)SP_EMPTY,
+                                       (unsigned long long)key);
+        if (old == SP_EMPTY) return 1;
+        if (old == key) return 0;
+        h = (h + 1) & (SP_H - 1);
+    }
+    return -1;
+}
+
+// idx == nullptr: productive indices [0, np) restricted to this shard's
+// batches (batch = i / B); else the n listed productive indices.
+template <bool STATS>
+__global__ void __launch_bounds__(SP_WARPS * 32) k_sparse(const DevAuto A, const uint32_t *__restrict__ cand,
+                                                          const uint32_t *__restrict__ pidx,
+                                                          const uint32_t *__restrict__ idx, uint64_t n, uint64_t B,
+                                                          uint32_t shard_index, uint32_t shard_count,
+                                                          unsigned long long *counts, uint8_t *overflow,
+                                                          unsigned long long *stats) {
+    __shared__ uint64_t tab_s[SP_WARPS][SP_H];
+    __shared__ uint64_t que_s[SP_WARPS][SP_Q];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    uint64_t *tab = tab_s[wl], *que = que_s[wl];
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned long long pe_acc = 0, src_done = 0;
+    for (uint64_t it = wid; it < n; it += nwarps) {
+        const uint64_t pi = idx ? idx[it] : it;
+        if (!idx && (pi / B) % shard_count != shard_index) continue;
+        const uint32_t s = cand[pidx[pi]];
+        for (int k = lane; k < SP_H; k += 32) tab[k] = SP_EMPTY;
+        __syncwarp();
+        unsigned long long cnt = 0, pe = 0;
+        bool ovf = false;
+        int head = 0, tail = 1;
+        if (lane == 0) {
+            sp_insert(tab, (uint64_t)s << 8);
+            que[0] = (uint64_t)s << 8;
+            if (A.final_mask & 1ull) { sp_insert(tab, ((uint64_t)s << 8) | 255u); cnt = 1; }
+        }
+        __syncwarp();
+        while (head < tail && !ovf) {
+            const uint64_t key = que[head++];
+            const uint32_t v = (uint32_t)(key >> 8), q = (uint32_t)(key & 0xff);
+            for (int t = A.toff[q]; t < A.toff[q + 1] && !ovf; ++t) {
+                const uint32_t q2 = A.tto[t];
+                const bool fin2 = (A.final_mask >> q2) & 1ull;
+                const bool live2 = A.toff[q2 + 1] > A.toff[q2];
+                const uint32_t *off = A.off[A.tslot[t]];
+                const uint32_t beg = __ldg(off + v), end = __ldg(off + v + 1);
+                pe += end - beg;
+                const uint32_t *nbr = A.nbr[A.tslot[t]];
+                for (uint32_t j = beg; j < end && !ovf; j += 32) {
+                    const bool valid = j + lane < end;
+                    const uint32_t w = valid ? __ldg(nbr + j + lane) : 0u;
+                    const int ins = valid ? sp_insert(tab, ((uint64_t)w << 8) | q2) : 0;
+                    if (__ballot_sync(0xffffffffu, ins < 0)) { ovf = true; break; }
+                    const unsigned newm = __ballot_sync(0xffffffffu, ins == 1);
+                    if (live2 && newm) {
+                        const int pos = tail + __popc(newm & lt);
+                        if (ins == 1 && pos < SP_Q) que[pos] = ((uint64_t)w << 8) | q2;
+                        tail += __popc(newm);
+                        if (tail > SP_Q) { ovf = true; break; }
+                    }
+                    if (fin2 && newm) {
+                        const int r2 = (ins == 1) ? sp_insert(tab, ((uint64_t)w << 8) | 255u) : 0;
+                        if (__ballot_sync(0xffffffffu, r2 < 0)) { ovf = true; break; }
+                        cnt += __popc(__ballot_sync(0xffffffffu, r2 == 1));
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        if (lane == 0) {
+            counts[pi] = ovf ? 0ull : cnt;
+            overflow[pi] = ovf ? 1 : 0;
+        }
+        if (!ovf) { pe_acc += pe; src_done++; }
+        __syncwarp();
+    }
+    if (STATS && lane == 0) {
+        if (pe_acc) atomicAdd(stats + S_PE, pe_acc);
+        if (src_done) atomicAdd(stats + S_ITEMS, src_done);
+    }
+}
+
+__global__ void k_gather_idx(const uint32_t *cand, const uint32_t *pidx, const uint32_t *list, uint64_t n,
+                             uint32_t *out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = cand[pidx[list[i]]];
+}
+
+// per-candidate counts from the sparse pass (non-overflowed sources)
+__global__ void k_sparse_scatter(const uint32_t *pidx, const unsigned long long *counts, const uint8_t *overflow,
+                                 uint64_t np, uint64_t B, uint32_t shard_index, uint32_t shard_count,
+                                 unsigned long long *cand_cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < np; i += (uint64_t)gridDim.x * blockDim.x)
+        if ((i / B) % shard_count == shard_index && !overflow[i]) cand_cnt[pidx[i]] = counts[i];
+}
+
+// per-candidate counts of a dense sub-evaluation (source ids -> candidate
+// indices by binary search in the sorted candidate list)
+__global__ void k_scatter_sub(const uint32_t *cand, uint64_t nsrc, const uint32_t *src, const unsigned long long *c,
+                              uint64_t n, unsigned long long *cand_cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = nsrc;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (cand[mid] < src[i]) lo = mid + 1; else hi = mid;
+        }
+        cand_cnt[lo] = c[i];
+    }
+}
+
 // ---- productive sources: s with an out-edge under a label leaving q0 ------
 __global__ void k_productive(const DevAuto A, const uint32_t *__restrict__ cand, uint64_t n, uint8_t *flag) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
@@ -661,8 +792,8 @@ __global__ void k_batch_bounds(const uint32_t *pidx, const uint32_t *cand, uint6
 // Dense clear of the batch state, only when the finished batch touched a
 // large fraction of it (device-side decision: no host round trip).
 __global__ void k_clear_dense(uint64_t *Vis, uint64_t *Done, uint64_t words, uint32_t *TX, uint64_t nxwords,
-                              uint32_t *TU, uint64_t ntu, const Ctrl *ctrl, uint64_t nunits) {
-    if ((uint64_t)ctrl->ntouched * 4 <= nunits) return;
+                              uint32_t *TU, uint64_t ntu, const Ctrl *ctrl, uint64_t nunits, int force_dense) {
+    if (!force_dense && (uint64_t)ctrl->ntouched * 4 <= nunits) return;
     const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = i0; i < words; i += st) { Vis[i] = 0; Done[i] = 0; }
     for (uint64_t i = i0; i < nxwords; i += st) TX[i] = 0;
@@ -692,8 +823,9 @@ __device__ __forceinline__ uint64_t ans_word(const DevAuto &A, const Layout &S, 
 
 // COUNT: total popcount of Ans over the hull [vlo, vlo + vn) x [0, nw).
 __global__ void k_count_total(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
-                              uint32_t nw, unsigned long long *total, const Ctrl *ctrl, uint64_t nunits) {
-    if (ctrl && (uint64_t)ctrl->ntouched * 4 <= nunits) return;   // sparse batch: k_count_touched counts
+                              uint32_t nw, unsigned long long *total, const Ctrl *ctrl, uint64_t nunits,
+                              int force_dense) {
+    if (!force_dense && ctrl && (uint64_t)ctrl->ntouched * 4 <= nunits) return;   // sparse: k_count_touched counts
     unsigned long long acc = 0;
     const uint64_t n = vn * nw;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -1088,6 +1220,12 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     bool q0_entered = false;
     for (size_t t = 0; t < a->to.size(); ++t) q0_entered |= a->to[t] == 0;
     const bool skip_q0 = a->nq > 0 && !q0_entered && !((a->final_mask >> 0) & 1ull) && !getenv("RPQ_NO_SKIP_Q0");
+    // a final state without outgoing transitions collects result bits
+    // without activity bitmaps, so its rows are not in the touched sets:
+    // such automata clear and count densely
+    int dead_final = 0;
+    for (uint32_t q = 0; q < a->nq; ++q)
+        if (((a->final_mask >> q) & 1ull) && a->off[q + 1] == a->off[q]) dead_final = 1;
 
     // ---- batch plan -------------------------------------------------------
     // Rows of the worst batch (q0 range = hull of all productive sources) set
@@ -1167,6 +1305,137 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     }
 
     PT.mark("batch plan");
+    std::vector<uint64_t> js;   // batch b owns candidates [js[b], js[b+1]) (plan.cpp)
+    batch_plan(bfirst.data(), nbatches, nsrc, js);
+    auto jstart = [&](uint64_t b) -> uint64_t { return js[b]; };
+    const uint64_t nb_eff = std::max<uint64_t>(nbatches, 1);
+
+    // ---- sparse engine: a warp per source when the per-source reach is
+    // small (decided on a sample); overflowing sources go to the dense engine
+    bool sparse_done = false;
+    uint64_t sparse_total = 0, sub_pe = 0;
+    unsigned long long *cand_cnt = nullptr;
+    unsigned long long *d_stats = (unsigned long long *)ws.get(NSTAT * 8 + 8);
+    if (!d_stats) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+    unsigned long long *d_total = d_stats + NSTAT;
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_stats, 0, NSTAT * 8 + 8, s));
+    {
+        const char *eng = getenv("RPQ_ENGINE");
+        const bool force_dense = (o.reserved & 1u) || (eng && !strcmp(eng, "dense"));
+        const bool force_sparse = eng && !strcmp(eng, "sparse");
+        if (np && !want_pairs && !force_dense) {
+            unsigned long long *sc = (unsigned long long *)ws.get(np * 8);
+            uint8_t *sov = (uint8_t *)ws.get(np);
+            if (!sc || !sov) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sparse)"));
+            bool use = force_sparse;
+            if (!use) {
+                const uint64_t ns = std::min<uint64_t>(np, 2048);
+                std::vector<uint32_t> hidx(ns);
+                for (uint64_t k = 0; k < ns; ++k) hidx[k] = (uint32_t)(k * np / ns);
+                uint32_t *didx = (uint32_t *)ws.get(ns * 4);
+                if (!didx) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                RPQ_CUDA_TRY(cudaMemcpyAsync(didx, hidx.data(), ns * 4, cudaMemcpyHostToDevice, s));
+                k_sparse<false><<<grid_for(ns * 32, SP_WARPS * 32, 148 * 8), SP_WARPS * 32, 0, s>>>(
+                    A, cand, pidx, didx, ns, B, 0, 1, sc, sov, d_stats);
+                ST.kernel_launches++;
+                std::vector<uint8_t> hov(np);
+                // flags of the sampled indices only
+                std::vector<uint8_t> all(np);
+                RPQ_CUDA_TRY(cudaMemcpyAsync(all.data(), sov, np, cudaMemcpyDeviceToHost, s));
+                RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                uint64_t nov = 0;
+                for (uint64_t k = 0; k < ns; ++k) nov += all[hidx[k]];
+                use = nov * 50 <= ns;   // <= 2 % of the sample overflows
+            }
+            if (use) {
+                // full pass over this shard's productive sources
+                RPQ_CUDA_TRY(cudaMemsetAsync(sc, 0, np * 8, s));
+                RPQ_CUDA_TRY(cudaMemsetAsync(sov, 0, np, s));
+                cudaEvent_t sp0 = nullptr, sp1 = nullptr;
+                if (timeit) { cudaEventCreate(&sp0); cudaEventCreate(&sp1); cudaEventRecord(sp0, s); }
+                if (stats)
+                    k_sparse<true><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B, o.shard_index,
+                                                                     shard_count, sc, sov, d_stats);
+                else
+                    k_sparse<false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B, o.shard_index,
+                                                                      shard_count, sc, sov, d_stats);
+                ST.kernel_launches++;
+                if (timeit) {
+                    cudaEventRecord(sp1, s);
+                    cudaEventSynchronize(sp1);
+                    float ms = 0;
+                    cudaEventElapsedTime(&ms, sp0, sp1);
+                    ST.expand_ms += ms;
+                    cudaEventDestroy(sp0);
+                    cudaEventDestroy(sp1);
+                }
+                ST.expand_launches += 1;
+                // overflowed sources -> dense sub-evaluation
+                uint32_t *olist = (uint32_t *)ws.get(np * 4);
+                uint64_t *d_no = (uint64_t *)ws.get(8);
+                unsigned long long *d_sum = (unsigned long long *)ws.get(8);
+                if (!olist || !d_no || !d_sum) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                size_t t1 = 0, t2 = 0;
+                thrust::counting_iterator<uint32_t> itc(0);
+                cub::DeviceSelect::Flagged(nullptr, t1, itc, sov, olist, d_no, (int64_t)np, s);
+                cub::DeviceReduce::Sum(nullptr, t2, sc, d_sum, (int64_t)np, s);
+                void *tmp = ws.get(std::max(t1, t2));
+                if (!tmp) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                cub::DeviceSelect::Flagged(tmp, t1, itc, sov, olist, d_no, (int64_t)np, s);
+                cub::DeviceReduce::Sum(tmp, t2, sc, d_sum, (int64_t)np, s);
+                uint64_t no = 0;
+                unsigned long long ssum = 0;
+                RPQ_CUDA_TRY(cudaMemcpyAsync(&no, d_no, 8, cudaMemcpyDeviceToHost, s));
+                RPQ_CUDA_TRY(cudaMemcpyAsync(&ssum, d_sum, 8, cudaMemcpyDeviceToHost, s));
+                RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                sparse_total = ssum;
+                // epsilon pairs of the non-productive candidates in this shard's batches
+                if (eps)
+                    for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count) {
+                        const uint64_t nbp = b < nbatches ? std::min<uint64_t>(B, np - b * B) : 0;
+                        sparse_total += (js[b + 1] - js[b]) - nbp;
+                    }
+                if (want_ps) {
+                    cand_cnt = (unsigned long long *)ws.get(std::max<uint64_t>(nsrc, 1) * 8);
+                    if (!cand_cnt) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (counts)"));
+                    k_fill_eps<<<grid_for(nsrc), 256, 0, s>>>(cand_cnt, nsrc, eps ? 1ull : 0ull);
+                    k_sparse_scatter<<<grid_for(np), 256, 0, s>>>(pidx, sc, sov, np, B, o.shard_index, shard_count,
+                                                                 cand_cnt);
+                    ST.kernel_launches += 2;
+                }
+                if (no) {
+                    uint32_t *osrc = (uint32_t *)ws.get(no * 4);
+                    if (!osrc) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                    k_gather_idx<<<grid_for(no), 256, 0, s>>>(cand, pidx, olist, no, osrc);
+                    ST.kernel_launches++;
+                    rpq_eval_opts so = o;
+                    so.reserved |= 1u;               // dense only
+                    so.shard_index = 0;
+                    so.shard_count = 1;
+                    so.mode = (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS)) | (want_ps ? RPQ_PER_SOURCE : RPQ_COUNT);
+                    rpq_result *sub = nullptr;
+                    rpq_status sst = eval_sources_device(g, a, osrc, no, &so, &sub);
+                    if (sst != RPQ_OK) return fail(sst);
+                    struct SubGuard { rpq_result *r; ~SubGuard() { rpq_result_release(r); } } sg{sub};
+                    sparse_total += sub->count;
+                    const rpq_stats &ss = sub->stats;
+                    ST.word_items += ss.word_items; ST.word_edge_ops += ss.word_edge_ops; ST.items += ss.items;
+                    ST.item_edges += ss.item_edges; ST.item_transitions += ss.item_transitions;
+                    ST.activations += ss.activations; ST.next_reds += ss.next_reds; ST.levels += ss.levels;
+                    ST.batches += ss.batches; ST.expand_launches += ss.expand_launches;
+                    ST.kernel_launches += ss.kernel_launches; ST.expand_ms += ss.expand_ms;
+                    sub_pe = ss.product_edges;
+                    if (want_ps && sub->n_ps) {
+                        k_scatter_sub<<<grid_for(sub->n_ps), 256, 0, s>>>(
+                            cand, nsrc, sub->ps_src, (const unsigned long long *)sub->ps_cnt, sub->n_ps, cand_cnt);
+                        ST.kernel_launches++;
+                    }
+                }
+                sparse_done = true;
+                ST.batches += 1;
+            }
+        }
+    }
     // ---- workspace ----------------------------------------------------------
     const uint64_t words = R_max * nw;
     ST.state_words = words;
@@ -1177,14 +1446,12 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     uint64_t *Vis = nullptr, *Done = nullptr, *hubF = nullptr;
     uint32_t *X0 = nullptr, *X1 = nullptr, *XB0 = nullptr, *XB1 = nullptr;
     Ctrl *ctrl = (Ctrl *)ws.get(sizeof(Ctrl));
-    unsigned long long *d_stats = (unsigned long long *)ws.get(NSTAT * 8 + 8);
-    unsigned long long *d_total = d_stats + NSTAT;
     // small pinned host word for the per-level flag readback (per thread)
     static thread_local uint32_t *h_cnt = nullptr;
     if (!h_cnt) RPQ_CUDA_TRY(cudaMallocHost(&h_cnt, 64));
     HubRec *hrecs = nullptr;
     HubItem *hitems = nullptr;
-    if (nbatches) {
+    if (nbatches && !sparse_done) {
         Vis = (uint64_t *)ws.get(words * 8);
         Done = (uint64_t *)ws.get(words * 8);
         X0 = (uint32_t *)ws.get(nxwords * 4 + 128);
@@ -1205,13 +1472,11 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaMemsetAsync(XB1, 0, xbwords * 4, s));
     }
     if (!ctrl || !d_stats) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory"));
-    RPQ_CUDA_TRY(cudaMemsetAsync(d_stats, 0, NSTAT * 8 + 8, s));
     RPQ_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s));
 
     PT.mark("workspace alloc + clear");
     // per-candidate counts (PER_SOURCE / PAIRS), initialised to the epsilon pair
-    unsigned long long *cand_cnt = nullptr;
-    if (want_ps) {
+    if (want_ps && !cand_cnt) {
         cand_cnt = (unsigned long long *)ws.get(std::max<uint64_t>(nsrc, 1) * 8);
         if (!cand_cnt) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (counts)"));
         k_fill_eps<<<grid_for(nsrc), 256, 0, s>>>(cand_cnt, nsrc, eps ? 1ull : 0ull);
@@ -1224,10 +1489,6 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     uint64_t total = 0;
     // candidate-index interval owned by batch b (non-productive candidates in
     // it contribute their epsilon pair); one virtual batch when P is empty
-    std::vector<uint64_t> js;   // batch b owns candidates [js[b], js[b+1]) (plan.cpp)
-    batch_plan(bfirst.data(), nbatches, nsrc, js);
-    auto jstart = [&](uint64_t b) -> uint64_t { return js[b]; };
-    const uint64_t nb_eff = std::max<uint64_t>(nbatches, 1);
 
     // ---- level loop setup: parity-0/1 argument sets and the device graph ----
     Layout *d_layout = (Layout *)ws.get(sizeof(Layout));
@@ -1259,7 +1520,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     const int lgrid = 148 * RPQ_LEVEL_MINB;   // persistent: warps fetch work units dynamically
     const int hgrid = 148 * RPQ_LEVEL_MINB;
     LevelGraph LG;
-    if (nbatches && !getenv("RPQ_HOST_LOOP")) {
+    if (nbatches && !sparse_done && !getenv("RPQ_HOST_LOOP")) {
         cudaError_t ge = stats ? build_level_graph<true>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords)
                                : build_level_graph<false>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords);
         if (ge != cudaSuccess) {   // fall back to the host-driven loop
@@ -1273,7 +1534,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     // layouts of this shard's batches, computed up front and copied once
     std::vector<Layout> lay_h;
     std::vector<Range> lay_fin;
-    for (uint64_t b = o.shard_index; b < nbatches; b += shard_count) {
+    for (uint64_t b = o.shard_index; b < (sparse_done ? 0 : nbatches); b += shard_count) {
         Layout S{};
         uint64_t rows = 0;
         Range fin_hull{1, 0};
@@ -1302,7 +1563,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *v;
         ~TevGuard() { for (auto &e : *v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); } }
     } tevg{&tev};
-    for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count) {
+    for (uint64_t b = o.shard_index; b < (sparse_done ? 0 : nb_eff); b += shard_count) {
         const uint64_t jlo = jstart(b), jhi = (b + 1 < nb_eff) ? jstart(b + 1) : nsrc;
         ST.batches++;
         if (b >= nbatches) {   // virtual batch: only epsilon pairs
@@ -1333,9 +1594,9 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         const Layout &S = lay_h[lay_i];
         const Range fin_hull = lay_fin[lay_i];
         if (lay_i > 0) {   // clear what the previous batch of this shard touched
-            k_clear_touched<<<148 * 8, 256, 0, s>>>(P0, nunits);
+            k_clear_touched<<<148 * 8, 256, 0, s>>>(P0, nunits, dead_final);
             k_clear_dense<<<148 * 8, 256, 0, s>>>(Vis, Done, words, TX, nxwords + 32, TU, (nunits + 31) / 32 + 1,
-                                                  ctrl, nunits);
+                                                  ctrl, nunits, dead_final);
             ST.kernel_launches += 2;
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, d_layouts + lay_i, sizeof(Layout), cudaMemcpyDeviceToDevice, s));
@@ -1374,9 +1635,9 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         if (!want_ps) {
             // COUNT: accumulate on the device (sparse or dense path chosen
             // there from the touched-unit count); no host round trip
-            k_count_touched<<<148 * 8, 256, 0, s>>>(A, S, P0, nunits, d_total);
+            k_count_touched<<<148 * 8, 256, 0, s>>>(A, S, P0, nunits, d_total, dead_final);
             if (vn) k_count_total<<<grid_for(vn * nw), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, d_total, ctrl,
-                                                                     nunits);
+                                                                     nunits, dead_final);
             ST.kernel_launches += vn ? 2 : 1;
             total += eps_np;
             continue;
@@ -1430,7 +1691,8 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaGetLastError());
     }
 
-    if (!want_ps && nbatches) {
+    if (sparse_done) total = sparse_total;
+    if (!want_ps && nbatches && !sparse_done) {
         unsigned long long t = 0;
         RPQ_CUDA_TRY(cudaMemcpyAsync(&t, d_total, 8, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1491,7 +1753,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         cub::DeviceSelect::FlaggedIf(tmp, tb2, cand, cand_cnt, res->ps_src, d_n, (int64_t)nsrc, NZ(), s);
         RPQ_CUDA_TRY(cudaMemcpyAsync(&res->n_ps, d_n, 8, cudaMemcpyDeviceToHost, s));
     }
-    if (nbatches) {
+    if (nbatches && !sparse_done) {
         Ctrl hc{};
         RPQ_CUDA_TRY(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1503,7 +1765,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         unsigned long long hs[NSTAT];
         RPQ_CUDA_TRY(cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        ST.product_edges = hs[S_PE];
+        ST.product_edges = hs[S_PE] + sub_pe;
         ST.word_items = hs[S_WORD_ITEMS];
         ST.word_edge_ops = hs[S_WORD_EDGE];
         ST.items = hs[S_ITEMS];

@@ -288,3 +288,48 @@ def test_ldbc_closed_forms(B):
     got[s] = c
     assert np.array_equal(got, want)
     assert R.rpq_eval_allpairs(G, k, mode=R.RPQ_COUNT, batch_sources=B).count == int(per.sum())
+
+
+@pytest.mark.parametrize("engine", ["sparse", "dense"])
+def test_engines_agree(engine, monkeypatch):
+    """The sparse (warp per source, shared-memory visited set) and dense
+    (bit-parallel) engines give identical counts, per-source counts and PE;
+    forcing the sparse engine on a dense query exercises the overflow
+    fallback to the dense engine."""
+    monkeypatch.setenv("RPQ_ENGINE", engine)
+    g = synth.random_graph(3000, 9000, 3, seed=21)
+    G = R.rpq_graph_load(g)
+    for rx in ["a b* c", "(a|b)*c*", "abc", "c?a"]:
+        want, o = oracle_rows(g, rx)
+        r = gpu_eval(G, rx, R.RPQ_PER_SOURCE | R.RPQ_STATS)
+        s, c = r.source_counts()
+        nz = o["counts"] > 0
+        assert np.array_equal(s, o["sources"][nz]) and np.array_equal(c, o["counts"][nz]), (engine, rx)
+        assert r.stats()["product_edges"] == int(o["pe"].sum()), (engine, rx)
+        for sc in [1, 3]:
+            tot = sum(gpu_eval(G, rx, R.RPQ_COUNT, batch_sources=512, shard_index=i, shard_count=sc).count
+                      for i in range(sc))
+            assert tot == want.shape[0], (engine, rx, sc)
+    # LDBC replyOf* (sparse reach) and knows+ (dense reach) under auto choice
+    monkeypatch.delenv("RPQ_ENGINE")
+    lg = synth.ldbc_graph(0.002)
+    LG = R.rpq_graph_load(lg)
+    depth = _reply_depths(lg)
+    r = gpu_eval(LG, "replyOf*", R.RPQ_COUNT | R.RPQ_STATS)
+    assert r.count == lg.num_vertices + int(depth.sum())
+
+
+def test_sparse_batches_dense_engine(monkeypatch):
+    """Many small batches with small reach take the touched-set clear/count
+    path of the dense engine; automata whose final state has no outgoing
+    transition must still count every result bit (they fall back to dense
+    clearing/counting)."""
+    monkeypatch.setenv("RPQ_ENGINE", "dense")
+    g = synth.random_graph(40000, 24000, 3, seed=22)
+    G = R.rpq_graph_load(g)
+    for rx in ["ab*c", "c?a", "abc", "(a|b)*c*", "a+", "b"]:
+        want, _ = oracle_rows(g, rx)
+        for B in [64, 256]:
+            assert gpu_eval(G, rx, R.RPQ_COUNT, batch_sources=B).count == want.shape[0], (rx, B)
+        r = gpu_eval(G, rx, R.RPQ_PAIRS, batch_sources=128)
+        assert_pairs_equal(r.rows(), want, rx)
