@@ -661,13 +661,18 @@ __device__ __forceinline__ int sp_insert(uint64_t *tab, uint64_t key) {
 
 // idx == nullptr: productive indices [0, np) restricted to this shard's
 // batches (batch = i / B); else the n listed productive indices.
-template <bool STATS>
+// WRITE: second pass of PAIRS mode -- re-run the BFS of every source that
+// did not overflow and write its distinct targets, sorted, at start[cand].
+template <bool STATS, bool WRITE>
 __global__ void __launch_bounds__(SP_WARPS * 32) k_sparse(const DevAuto A, const uint32_t *__restrict__ cand,
                                                           const uint32_t *__restrict__ pidx,
                                                           const uint32_t *__restrict__ idx, uint64_t n, uint64_t B,
                                                           uint32_t shard_index, uint32_t shard_count,
                                                           unsigned long long *counts, uint8_t *overflow,
-                                                          unsigned long long *stats) {
+                                                          unsigned long long *stats,
+                                                          const unsigned long long *start = nullptr,
+                                                          uint32_t *osrc = nullptr, uint32_t *odst = nullptr,
+                                                          int *err = nullptr) {
     __shared__ uint64_t tab_s[SP_WARPS][SP_H];
     __shared__ uint64_t que_s[SP_WARPS][SP_Q];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
@@ -679,6 +684,7 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_sparse(const DevAuto A, const
     for (uint64_t it = wid; it < n; it += nwarps) {
         const uint64_t pi = idx ? idx[it] : it;
         if (!idx && (pi / B) % shard_count != shard_index) continue;
+        if (WRITE && overflow[pi]) continue;
         const uint32_t s = cand[pidx[pi]];
         for (int k = lane; k < SP_H; k += 32) tab[k] = SP_EMPTY;
         __syncwarp();
@@ -723,14 +729,41 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_sparse(const DevAuto A, const
                 __syncwarp();
             }
         }
-        if (lane == 0) {
-            counts[pi] = ovf ? 0ull : cnt;
-            overflow[pi] = ovf ? 1 : 0;
+        if constexpr (WRITE) {
+            if (ovf) {   // the first pass fitted; a different probe order did not
+                if (lane == 0) atomicExch(err, 1);
+                continue;
+            }
+            // gather the target markers (v, 255) and write them ranked
+            uint32_t *lst = reinterpret_cast<uint32_t *>(que);
+            int nl = 0;
+            for (int k0 = 0; k0 < SP_H; k0 += 32) {
+                const uint64_t key = tab[k0 + lane];
+                const bool mk = key != SP_EMPTY && (key & 0xff) == 255u;
+                const unsigned mm = __ballot_sync(0xffffffffu, mk);
+                if (mk) lst[nl + __popc(mm & lt)] = (uint32_t)(key >> 8);
+                nl += __popc(mm);
+            }
+            __syncwarp();
+            const unsigned long long base = start[pidx[pi]];
+            for (int i = lane; i < nl; i += 32) {
+                const uint32_t t = lst[i];
+                int r = 0;
+                for (int j = 0; j < nl; ++j) r += lst[j] < t;
+                osrc[base + r] = s;
+                odst[base + r] = t;
+            }
+            __syncwarp();
+        } else {
+            if (lane == 0) {
+                counts[pi] = ovf ? 0ull : cnt;
+                overflow[pi] = ovf ? 1 : 0;
+            }
+            if (!ovf) { pe_acc += pe; src_done++; }
         }
-        if (!ovf) { pe_acc += pe; src_done++; }
         __syncwarp();
     }
-    if (STATS && lane == 0) {
+    if (STATS && !WRITE && lane == 0) {
         if (pe_acc) atomicAdd(stats + S_PE, pe_acc);
         if (src_done) atomicAdd(stats + S_ITEMS, src_done);
     }
@@ -748,6 +781,29 @@ __global__ void k_sparse_scatter(const uint32_t *pidx, const unsigned long long 
                                  unsigned long long *cand_cnt) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < np; i += (uint64_t)gridDim.x * blockDim.x)
         if ((i / B) % shard_count == shard_index && !overflow[i]) cand_cnt[pidx[i]] = counts[i];
+}
+
+// pairs of a dense sub-evaluation (sorted by source; sstart = scan of its
+// per-source counts) copied to their places in the sparse PAIRS output
+__global__ void k_place_sub(const uint32_t *cand, uint64_t nsrc, const uint32_t *ps_src,
+                            const unsigned long long *ps_cnt, const unsigned long long *sstart, uint64_t n,
+                            const uint32_t *ssrc, const uint32_t *sdst, const unsigned long long *start,
+                            uint32_t *osrc, uint32_t *odst) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    for (uint64_t i = wid; i < n; i += nwarps) {
+        uint64_t lo = 0, hi = nsrc;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (cand[mid] < ps_src[i]) lo = mid + 1; else hi = mid;
+        }
+        const unsigned long long o = start[lo], a = sstart[i], c = ps_cnt[i];
+        for (unsigned long long k = lane; k < c; k += 32) {
+            osrc[o + k] = ssrc[a + k];
+            odst[o + k] = sdst[a + k];
+        }
+    }
 }
 
 // per-candidate counts of a dense sub-evaluation (source ids -> candidate
@@ -1314,6 +1370,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     // small (decided on a sample); overflowing sources go to the dense engine
     bool sparse_done = false;
     uint64_t sparse_total = 0, sub_pe = 0;
+    rpq_result *sub_keep = nullptr;
     unsigned long long *cand_cnt = nullptr;
     unsigned long long *d_stats = (unsigned long long *)ws.get(NSTAT * 8 + 8);
     if (!d_stats) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
@@ -1323,7 +1380,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         const char *eng = getenv("RPQ_ENGINE");
         const bool force_dense = (o.reserved & 1u) || (eng && !strcmp(eng, "dense"));
         const bool force_sparse = eng && !strcmp(eng, "sparse");
-        if (np && !want_pairs && !force_dense) {
+        if (np && !force_dense) {
             unsigned long long *sc = (unsigned long long *)ws.get(np * 8);
             uint8_t *sov = (uint8_t *)ws.get(np);
             if (!sc || !sov) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sparse)"));
@@ -1335,7 +1392,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
                 uint32_t *didx = (uint32_t *)ws.get(ns * 4);
                 if (!didx) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
                 RPQ_CUDA_TRY(cudaMemcpyAsync(didx, hidx.data(), ns * 4, cudaMemcpyHostToDevice, s));
-                k_sparse<false><<<grid_for(ns * 32, SP_WARPS * 32, 148 * 8), SP_WARPS * 32, 0, s>>>(
+                k_sparse<false, false><<<grid_for(ns * 32, SP_WARPS * 32, 148 * 8), SP_WARPS * 32, 0, s>>>(
                     A, cand, pidx, didx, ns, B, 0, 1, sc, sov, d_stats);
                 ST.kernel_launches++;
                 std::vector<uint8_t> hov(np);
@@ -1354,10 +1411,10 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
                 cudaEvent_t sp0 = nullptr, sp1 = nullptr;
                 if (timeit) { cudaEventCreate(&sp0); cudaEventCreate(&sp1); cudaEventRecord(sp0, s); }
                 if (stats)
-                    k_sparse<true><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B, o.shard_index,
+                    k_sparse<true, false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B, o.shard_index,
                                                                      shard_count, sc, sov, d_stats);
                 else
-                    k_sparse<false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B, o.shard_index,
+                    k_sparse<false, false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B, o.shard_index,
                                                                       shard_count, sc, sov, d_stats);
                 ST.kernel_launches++;
                 if (timeit) {
@@ -1412,7 +1469,8 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
                     so.reserved |= 1u;               // dense only
                     so.shard_index = 0;
                     so.shard_count = 1;
-                    so.mode = (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS)) | (want_ps ? RPQ_PER_SOURCE : RPQ_COUNT);
+                    so.mode = (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS)) |
+                              (want_pairs ? RPQ_PAIRS : want_ps ? RPQ_PER_SOURCE : RPQ_COUNT);
                     rpq_result *sub = nullptr;
                     rpq_status sst = eval_sources_device(g, a, osrc, no, &so, &sub);
                     if (sst != RPQ_OK) return fail(sst);
@@ -1430,6 +1488,76 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
                             cand, nsrc, sub->ps_src, (const unsigned long long *)sub->ps_cnt, sub->n_ps, cand_cnt);
                         ST.kernel_launches++;
                     }
+                    if (want_pairs) {   // keep the sub-result until its pairs are placed
+                        sub_keep = sub;
+                        sg.r = nullptr;
+                    }
+                }
+                if (want_pairs) {
+                    // starts of every candidate (other shards' intervals count 0)
+                    for (uint64_t b = 0; b < nb_eff; ++b)
+                        if (b % shard_count != o.shard_index && js[b + 1] > js[b])
+                            RPQ_CUDA_TRY(cudaMemsetAsync(cand_cnt + js[b], 0, (js[b + 1] - js[b]) * 8, s));
+                    unsigned long long *start = (unsigned long long *)ws.get((nsrc + 1) * 8);
+                    int *d_err = (int *)ws.get(sizeof(int));
+                    if (!start || !d_err) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                    size_t tb = 0;
+                    cub::DeviceScan::ExclusiveSum(nullptr, tb, cand_cnt, start, (int64_t)nsrc, s);
+                    void *tmp2 = ws.get(tb);
+                    if (!tmp2) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                    cub::DeviceScan::ExclusiveSum(tmp2, tb, cand_cnt, start, (int64_t)nsrc, s);
+                    unsigned long long ls = 0, lc = 0;
+                    RPQ_CUDA_TRY(cudaMemcpyAsync(&ls, start + nsrc - 1, 8, cudaMemcpyDeviceToHost, s));
+                    RPQ_CUDA_TRY(cudaMemcpyAsync(&lc, cand_cnt + nsrc - 1, 8, cudaMemcpyDeviceToHost, s));
+                    RPQ_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
+                    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                    const uint64_t tot = ls + lc;
+                    res->ncols = 2;
+                    res->nrows = tot;
+                    if (cudaMalloc(&res->cols[0], std::max<uint64_t>(tot, 1) * 4) != cudaSuccess ||
+                        cudaMalloc(&res->cols[1], std::max<uint64_t>(tot, 1) * 4) != cudaSuccess) {
+                        cudaGetLastError();
+                        rpq_result_release(sub_keep);
+                        return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (%llu pairs)", (unsigned long long)tot));
+                    }
+                    k_sparse<false, true><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B,
+                                                                            o.shard_index, shard_count, sc, sov,
+                                                                            d_stats, start, res->cols[0],
+                                                                            res->cols[1], d_err);
+                    ST.kernel_launches++;
+                    if (sub_keep && sub_keep->n_ps) {
+                        unsigned long long *ss = (unsigned long long *)ws.get(sub_keep->n_ps * 8);
+                        size_t tb3 = 0;
+                        cub::DeviceScan::ExclusiveSum(nullptr, tb3, (unsigned long long *)sub_keep->ps_cnt, ss,
+                                                      (int64_t)sub_keep->n_ps, s);
+                        void *tmp3 = ws.get(tb3);
+                        if (!ss || !tmp3) { rpq_result_release(sub_keep); return fail(rpq_fail(RPQ_ENOMEM, "oom")); }
+                        cub::DeviceScan::ExclusiveSum(tmp3, tb3, (unsigned long long *)sub_keep->ps_cnt, ss,
+                                                      (int64_t)sub_keep->n_ps, s);
+                        k_place_sub<<<grid_for(sub_keep->n_ps * 32), 256, 0, s>>>(
+                            cand, nsrc, sub_keep->ps_src, (const unsigned long long *)sub_keep->ps_cnt, ss,
+                            sub_keep->n_ps, sub_keep->cols[0], sub_keep->cols[1], start, res->cols[0], res->cols[1]);
+                        ST.kernel_launches += 2;
+                    }
+                    if (eps)
+                        for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count)
+                            if (js[b + 1] > js[b]) {
+                                k_write_eps<<<grid_for(js[b + 1] - js[b]), 256, 0, s>>>(
+                                    flag, cand, js[b], js[b + 1], start + js[b], res->cols[0], res->cols[1]);
+                                ST.kernel_launches++;
+                            }
+                    int herr = 0;
+                    RPQ_CUDA_TRY(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
+                    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                    rpq_result_release(sub_keep);
+                    sub_keep = nullptr;
+                    if (herr) {   // rare: redo the whole query on the dense engine
+                        rpq_eval_opts d = o;
+                        d.reserved |= 1u;
+                        rpq_result_release(res);
+                        return eval_sources_device(g, a, d_cand_in, nsrc, &d, out);
+                    }
+                    sparse_total = tot;   // pairs already include epsilon pairs
                 }
                 sparse_done = true;
                 ST.batches += 1;
@@ -1707,7 +1835,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     PT.mark("extraction");
     // ---- result assembly ---------------------------------------------------
     res->count = total;
-    if (want_pairs) {
+    if (want_pairs && !sparse_done) {
         res->ncols = 2;
         res->nrows = total;
         if (blocks.size() == 1) {

@@ -306,6 +306,12 @@ def test_engines_agree(engine, monkeypatch):
         nz = o["counts"] > 0
         assert np.array_equal(s, o["sources"][nz]) and np.array_equal(c, o["counts"][nz]), (engine, rx)
         assert r.stats()["product_edges"] == int(o["pe"].sum()), (engine, rx)
+        assert_pairs_equal(gpu_eval(G, rx, R.RPQ_PAIRS).rows(), want, (engine, rx))
+        parts = [gpu_eval(G, rx, R.RPQ_PAIRS, batch_sources=700, shard_index=i, shard_count=2).rows()
+                 for i in range(2)]
+        got = np.concatenate(parts)
+        got = got[np.lexsort((got[:, 1], got[:, 0]))]
+        assert_pairs_equal(got, want, (engine, rx, "sharded"))
         for sc in [1, 3]:
             tot = sum(gpu_eval(G, rx, R.RPQ_COUNT, batch_sources=512, shard_index=i, shard_count=sc).count
                       for i in range(sc))
