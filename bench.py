@@ -86,6 +86,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("BENCH_NOCLK") == "1":
+            return self
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -199,7 +201,7 @@ def run_ours(args):
 
     # timed steps run without the in-kernel counters; the algorithmic bytes
     # of a step come from the RPQ_STATS probe runs above (per query)
-    mode = R.RPQ_COUNT | R.RPQ_TIME_KERNELS
+    mode = R.RPQ_COUNT | (R.RPQ_TIME_KERNELS if os.environ.get("BENCH_TK", "1") == "1" else 0)
     probe_bytes = sum(algorithmic_bytes(probe[rx]) for rx in queries)
     probe_levels = sum(probe[rx]["levels"] for rx in queries)
     probe_pe = sum(probe[rx]["product_edges"] for rx in queries)
@@ -213,7 +215,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            flush.fill_(1)                       # evict L2 between timed steps (untimed)
+            if os.environ.get("BENCH_NOFLUSH") != "1":
+                flush.fill_(1)                   # evict L2 between timed steps (untimed)
             torch.cuda.synchronize()
             ev0.record(stream)
             t = step(mode)
@@ -228,6 +231,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    if os.environ.get("BENCH_DEBUG"):
+        print("step ms:", " ".join(f"{t:.1f}" for t in times), file=sys.stderr)
     total_ms = float(sum(times))
     pe_total = probe_pe * args.steps          # PE is a property of (graph, query, shard)
     if world > 1:

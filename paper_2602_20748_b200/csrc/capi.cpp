@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstring>
+#include <chrono>
 #include <mutex>
 
 #include "internal.h"
@@ -63,18 +64,50 @@ void *dev_alloc(size_t bytes, void *stream) {
 
 // Bytes an evaluation can still allocate: free device memory plus what the
 // stream-ordered pool has reserved but is not using (it keeps freed blocks).
-uint64_t dev_available() {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); return 0; }
+// cudaMemGetInfo is a driver (RM) call that was measured to stall for up to
+// ~90 ms on the B200 boxes, so the value is cached per device; it is
+// refreshed after 30 s, by graph load/free, and by an evaluation that ran out
+// of memory under a cached budget (eval_sources_device retries once).
+namespace {
+struct MemCache {
+    std::mutex m;
+    bool valid = false;
+    uint64_t bytes = 0;
+    std::chrono::steady_clock::time_point t;
+};
+MemCache g_memcache[64];
+}  // namespace
+
+uint64_t dev_available(bool *cached) {
     int dev = 0;
     cudaGetDevice(&dev);
+    MemCache &c = g_memcache[dev & 63];
+    std::lock_guard<std::mutex> lk(c.m);
+    const auto now = std::chrono::steady_clock::now();
+    if (c.valid && now - c.t < std::chrono::seconds(30)) {
+        if (cached) *cached = true;
+        return c.bytes;
+    }
+    if (cached) *cached = false;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); return 0; }
     cudaMemPool_t pool;
     uint64_t reserved = 0, used = 0;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
     }
-    return (uint64_t)free_b + (reserved > used ? reserved - used : 0);
+    c.bytes = (uint64_t)free_b + (reserved > used ? reserved - used : 0);
+    c.t = now;
+    c.valid = true;
+    return c.bytes;
+}
+
+void dev_available_invalidate() {
+    for (MemCache &c : g_memcache) {
+        std::lock_guard<std::mutex> lk(c.m);
+        c.valid = false;
+    }
 }
 
 void dev_free(void *p, void *stream) {

@@ -426,15 +426,24 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
     const uint32_t nunits = *(volatile uint32_t *)&p.ctrl->ucnt[p.par];
     unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
     bool act = false;
-    (void)wid; (void)nwarps;
+    (void)wid;
+    // Few active units (small row counts, e.g. knows+ over 65 K persons, or
+    // the narrow first/last levels): split each unit into 2^ls tickets of
+    // 32 >> ls X words so that every warp of the grid gets work; a ticket is
+    // one atomic on the level's cursor.
+    int ls = 0;
+    while (ls < 5 && ((uint64_t)nunits << ls) < nwarps * 8) ++ls;
+    const uint32_t ntk = nunits << ls;
+    const int part_lanes = 32 >> ls;
     for (;;) {
-        uint32_t ui = 0;
-        if (lane == 0) ui = atomicAdd(&p.ctrl->ucur[p.par], 1u);
-        ui = __shfl_sync(0xffffffffu, ui, 0);
-        if (ui >= nunits) break;
-        const uint64_t u = p.ulist[ui];
+        uint32_t tk = 0;
+        if (lane == 0) tk = atomicAdd(&p.ctrl->ucur[p.par], 1u);
+        tk = __shfl_sync(0xffffffffu, tk, 0);
+        if (tk >= ntk) break;
+        const uint64_t u = p.ulist[tk >> ls];
+        const bool mine = (lane / part_lanes) == (int)(tk & ((1u << ls) - 1u));
         const uint64_t xi_l = u * 32 + lane;
-        const uint32_t xl = xi_l < p.nxwords ? __ldcg(p.Xcur + xi_l) : 0u;
+        const uint32_t xl = (mine && xi_l < p.nxwords) ? __ldcg(p.Xcur + xi_l) : 0u;
         if (xl) {
             p.Xcur[xi_l] = 0u;
             p.TX[xi_l] |= xl;          // single owner per level; levels are ordered
@@ -1041,20 +1050,41 @@ __global__ void k_write_eps(const uint8_t *flag, const uint32_t *cand, uint64_t 
     }
 }
 
-// RPQ_DEBUG_TIMING=1: print host-observed phase times (synchronising)
+// RPQ_DEBUG_TIMING=1: print host-observed phase times (synchronising);
+// RPQ_DEBUG_EVENTS=1: device-side phase times from events (no synchronisation),
+// printed when the evaluation ends
 struct PhaseTimer {
-    bool on;
+    bool on, ev;
     cudaStream_t s;
     std::chrono::steady_clock::time_point t;
-    explicit PhaseTimer(cudaStream_t st) : on(getenv("RPQ_DEBUG_TIMING") != nullptr), s(st) {
+    std::vector<std::pair<const char *, cudaEvent_t>> evs;
+    explicit PhaseTimer(cudaStream_t st)
+        : on(getenv("RPQ_DEBUG_TIMING") != nullptr), ev(getenv("RPQ_DEBUG_EVENTS") != nullptr), s(st) {
         t = std::chrono::steady_clock::now();
+        mark("begin");
     }
     void mark(const char *what) {
+        if (ev) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, s);
+            evs.emplace_back(what, e);
+        }
         if (!on) return;
         cudaStreamSynchronize(s);
         auto n = std::chrono::steady_clock::now();
         fprintf(stderr, "[rpq] %-28s %9.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
         t = n;
+    }
+    ~PhaseTimer() {
+        if (!ev) return;
+        cudaStreamSynchronize(s);
+        for (size_t i = 1; i < evs.size(); ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, evs[i - 1].second, evs[i].second);
+            fprintf(stderr, "[rpq-ev] %-28s %9.3f ms\n", evs[i].first, ms);
+        }
+        for (auto &e : evs) cudaEventDestroy(e.second);
     }
 };
 
@@ -1182,8 +1212,8 @@ rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &
 
 // Evaluate the RPQ from the sorted, distinct candidate sources cand[0..nsrc)
 // (device array).  cand == nullptr means all of V (all-pairs, reading R11).
-rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint32_t *d_cand_in, uint64_t nsrc,
-                               const rpq_eval_opts *opts_in, rpq_result **out) {
+static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const uint32_t *d_cand_in, uint64_t nsrc,
+                                    const rpq_eval_opts *opts_in, rpq_result **out, bool *budget_cached) {
     rpq_eval_opts o{};
     if (opts_in) o = *opts_in;
     if (o.mode == 0) o.mode = RPQ_COUNT;
@@ -1209,6 +1239,16 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     EvGuard eg{evs};
     cudaEventRecord(e_begin, s);
     PhaseTimer PT(s);
+    // RPQ_DEBUG_HOST=1: report host calls of the driver that take > 1 ms
+    const bool dbg_host = getenv("RPQ_DEBUG_HOST") != nullptr;
+    auto h_t = std::chrono::steady_clock::now();
+    auto HM = [&](const char *what) {
+        if (!dbg_host) return;
+        auto n = std::chrono::steady_clock::now();
+        double ms = std::chrono::duration<double, std::milli>(n - h_t).count();
+        if (ms > 1.0) fprintf(stderr, "[rpq-host] %-28s %9.3f ms\n", what, ms);
+        h_t = n;
+    };
     rpq_stats &ST = res->stats;
 
     // ---- device automaton ------------------------------------------------
@@ -1256,6 +1296,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         cub::DeviceSelect::Flagged(tmp, tb, it, flag, pidx, d_np, (int64_t)nsrc, s);
         RPQ_CUDA_TRY(cudaMemcpyAsync(&np, d_np, 8, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        HM("np readback");
     } else if (nsrc) {
         RPQ_CUDA_TRY(cudaMemsetAsync(flag, 0, nsrc, s));
     }
@@ -1294,13 +1335,15 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaMemcpy(&p_first, cand + j0, 4, cudaMemcpyDeviceToHost));
         RPQ_CUDA_TRY(cudaMemcpy(&p_last, cand + j1, 4, cudaMemcpyDeviceToHost));
     }
+    HM("p_first/p_last");
     uint64_t R_max = 0;
     for (uint32_t q = 0; q < a->nq; ++q) {
         Range r = in_range[q];
         if (q == 0 && np && !skip_q0) r = hull(r, Range{p_first, p_last});
         R_max += r.empty() ? 0 : (uint64_t)r.hi - r.lo + 1;
     }
-    uint64_t budget = o.hbm_budget_bytes ? o.hbm_budget_bytes : (uint64_t)(dev_available() * 0.9);
+    uint64_t budget = o.hbm_budget_bytes ? o.hbm_budget_bytes : (uint64_t)(dev_available(budget_cached) * 0.9);
+    HM("dev_available");
     uint64_t B = o.batch_sources;
     if (B == 0) {
         // bytes per 64-source word column: Vis + Done, bitmaps, and for
@@ -1359,6 +1402,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
             sfirst[b] = hb[4 * b + 2]; slast[b] = hb[4 * b + 3];
         }
     }
+    HM("batch bounds");
 
     PT.mark("batch plan");
     std::vector<uint64_t> js;   // batch b owns candidates [js[b], js[b+1]) (plan.cpp)
@@ -1401,6 +1445,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
                 RPQ_CUDA_TRY(cudaMemcpyAsync(all.data(), sov, np, cudaMemcpyDeviceToHost, s));
                 RPQ_CUDA_TRY(cudaStreamSynchronize(s));
                 uint64_t nov = 0;
+                HM("sparse sample");
                 for (uint64_t k = 0; k < ns; ++k) nov += all[hidx[k]];
                 use = nov * 50 <= ns;   // <= 2 % of the sample overflows
             }
@@ -1599,6 +1644,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaMemsetAsync(XB0, 0, xbwords * 4, s));
         RPQ_CUDA_TRY(cudaMemsetAsync(XB1, 0, xbwords * 4, s));
     }
+    HM("state alloc+memset");
     if (!ctrl || !d_stats) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory"));
     RPQ_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), s));
 
@@ -1658,6 +1704,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         }
     }
     PT.mark("level graph");
+    HM("level graph");
 
     // layouts of this shard's batches, computed up front and copied once
     std::vector<Layout> lay_h;
@@ -1685,12 +1732,22 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
     }
     RPQ_CUDA_TRY(cudaMemsetAsync(d_total, 0, 8, s));
+        HM("layouts");
     size_t lay_i = 0;
+    // level-loop timing events (RPQ_TIME_KERNELS), recycled per thread
+    static thread_local std::vector<cudaEvent_t> ev_pool;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
+    auto take_ev = [&]() {
+        cudaEvent_t e = nullptr;
+        if (!ev_pool.empty()) { e = ev_pool.back(); ev_pool.pop_back(); }
+        else cudaEventCreate(&e);
+        return e;
+    };
     struct TevGuard {
         std::vector<std::pair<cudaEvent_t, cudaEvent_t>> *v;
-        ~TevGuard() { for (auto &e : *v) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); } }
-    } tevg{&tev};
+        std::vector<cudaEvent_t> *pool;
+        ~TevGuard() { for (auto &e : *v) { pool->push_back(e.first); pool->push_back(e.second); } }
+    } tevg{&tev, &ev_pool};
     for (uint64_t b = o.shard_index; b < (sparse_done ? 0 : nb_eff); b += shard_count) {
         const uint64_t jlo = jstart(b), jhi = (b + 1 < nb_eff) ? jstart(b + 1) : nsrc;
         ST.batches++;
@@ -1741,9 +1798,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         PT.mark("seed");
         rpq_status st = RPQ_OK;
         if (timeit) {
-            tev.emplace_back();
-            cudaEventCreate(&tev.back().first);
-            cudaEventCreate(&tev.back().second);
+            tev.emplace_back(take_ev(), take_ev());
             cudaEventRecord(tev.back().first, s);
         }
         if (LG.exec) {
@@ -1754,6 +1809,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         }
         if (timeit) cudaEventRecord(tev.back().second, s);
         PT.mark("levels");
+        HM("levels enqueued");
         if (st != RPQ_OK) return fail(st);
         // X and XB are all zero again here (the last level activated
         // nothing).  Extraction reads Vis of the final states.
@@ -1833,6 +1889,7 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
         ST.expand_ms += ms;
     }
     PT.mark("extraction");
+    HM("extraction+readback");
     // ---- result assembly ---------------------------------------------------
     res->count = total;
     if (want_pairs && !sparse_done) {
@@ -1908,9 +1965,23 @@ rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint3
     cudaEventElapsedTime(&tms, e_begin, e_end);
     ST.total_ms = tms;
     PT.mark("assembly");
+    HM("assembly");
     RPQ_CUDA_TRY(cudaGetLastError());
     *out = res;
     return RPQ_OK;
+}
+
+// The automatic batch width comes from a cached free-memory figure; if the
+// evaluation runs out of memory under it, refresh the figure and retry once.
+rpq_status eval_sources_device(const rpq_graph *g, const rpq_nfa *a, const uint32_t *d_cand_in, uint64_t nsrc,
+                               const rpq_eval_opts *opts_in, rpq_result **out) {
+    bool cached = false;
+    rpq_status st = eval_sources_impl(g, a, d_cand_in, nsrc, opts_in, out, &cached);
+    if (st == RPQ_ENOMEM && cached) {
+        dev_available_invalidate();
+        st = eval_sources_impl(g, a, d_cand_in, nsrc, opts_in, out, &cached);
+    }
+    return st;
 }
 
 // ---- public entry points ----------------------------------------------------

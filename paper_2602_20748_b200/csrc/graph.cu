@@ -78,6 +78,7 @@ extern "C" void rpq_graph_free(rpq_graph *g) {
     for (auto &c : g->csr) { cudaFree(c.off); cudaFree(c.nbr); }
     if (g->vlabel) cudaFree(g->vlabel);
     delete g;
+    dev_available_invalidate();
 }
 
 extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
@@ -207,6 +208,7 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return fail(RPQ_ECUDA, cudaGetErrorString(e));
     *out = g;
+    dev_available_invalidate();
     return RPQ_OK;
 }
 

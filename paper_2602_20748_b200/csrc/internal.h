@@ -62,7 +62,8 @@ struct rpq_result {
 // ---- device memory (stream-ordered pool allocator) -----------------------
 void *dev_alloc(size_t bytes, void *stream);          // nullptr on failure
 void dev_free(void *p, void *stream);
-uint64_t dev_available();                             // free + pool-reserved-unused bytes
+uint64_t dev_available(bool *cached = nullptr);       // free + pool-reserved-unused bytes (cached)
+void dev_available_invalidate();
 void rpq_result_release(rpq_result *r);
 
 // ---- evaluation driver (eval.cu) -----------------------------------------
