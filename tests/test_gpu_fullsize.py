@@ -1,0 +1,144 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration
+bench.py times (auto batch width, its shard layout).
+
+* cfg3 (LDBC-shaped, SF10 size): replyOf* and knows+ per-source counts for
+  ALL 35.5 M sources against the closed forms of SURVEY §8(c) (ancestor chain
+  + epsilon pair; connected-component size), plus COUNT totals.
+* cfg4 (same graph): the CRPQ m-hasTag->Sports, m-hasCreator->u,
+  m-replyOf*->p:Post against its closed form (one tuple per Sports-tagged
+  message) and, on a seeded sample of tuples, against O1 atom relations.
+* cfg5 (R-MAT scale 24, 268 M edge samples): bench.py's 1-GPU workload is
+  shard 0 of 16; its COUNT total must equal the sum of per-source counts over
+  the same sources (evaluated again at half the batch width, shards 0 and 1
+  of 32 = the same source set), and a seeded sample of those per-source
+  counts must equal O1's.
+
+Expected values come from the generators' own structure (closed forms) or
+from oracle/ -- never from the CUDA path.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+R = pytest.importorskip("paper_2602_20748_b200")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if R.rpq_device_count() == 0:
+        pytest.skip("no CUDA device")
+
+
+def reply_depths(g):
+    """Number of replyOf hops from each comment to its root post (the forest
+    is built with parents strictly earlier, so a fixed point of vectorised
+    passes is exact)."""
+    base, cnt = g.meta["base"], g.meta["count"]
+    C = cnt["Comment"]
+    pc = g.meta["reply_parent"] - base["Comment"]
+    is_c = (pc >= 0) & (pc < C)
+    pcc = np.where(is_c, pc, 0)
+    depth = np.ones(C, np.int64)
+    while True:
+        nd = 1 + np.where(is_c, depth[pcc], 0)
+        if np.array_equal(nd, depth):
+            return depth
+        depth = nd
+
+
+@pytest.fixture(scope="module")
+def ldbc():
+    g = synth.ldbc_graph(1.0, seed=10)          # bench.py --workload cfg3
+    G = R.rpq_graph_load(g)
+    return g, G
+
+
+def test_cfg3_sf10_closed_forms(ldbc):
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import connected_components
+    g, G = ldbc
+    base, cnt = g.meta["base"], g.meta["count"]
+    # replyOf*: every vertex has its epsilon pair (R1); a comment also reaches
+    # each ancestor up to and including its root post
+    depth = reply_depths(g)
+    want = np.ones(g.num_vertices, np.uint64)
+    want[base["Comment"]:base["Comment"] + cnt["Comment"]] += depth.astype(np.uint64)
+    a = R.rpq_compile(G, "replyOf*")
+    assert R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT).count == int(want.sum())
+    s, c = R.rpq_eval_allpairs(G, a, mode=R.RPQ_PER_SOURCE).source_counts()
+    assert np.array_equal(s, np.arange(g.num_vertices, dtype=s.dtype))
+    assert np.array_equal(c, want)
+    # knows+: symmetric, no self-loops -> per person the size of its
+    # connected component if that has >= 2 persons
+    P = cnt["Person"]
+    m = g.label == g.label_names.index("knows")
+    A = sp.csr_matrix((np.ones(int(m.sum())), (g.src[m] - base["Person"], g.dst[m] - base["Person"])), shape=(P, P))
+    _, comp = connected_components(A, directed=False)
+    sizes = np.bincount(comp)
+    per = np.where(sizes[comp] >= 2, sizes[comp], 0).astype(np.uint64)
+    k = R.rpq_compile(G, "knows+")
+    assert R.rpq_eval_allpairs(G, k, mode=R.RPQ_COUNT).count == int(per.sum())
+    s, c = R.rpq_eval_allpairs(G, k, mode=R.RPQ_PER_SOURCE).source_counts()
+    got = np.zeros(g.num_vertices, np.uint64)
+    got[s] = c
+    want_k = np.zeros(g.num_vertices, np.uint64)
+    want_k[base["Person"]:base["Person"] + P] = per
+    assert np.array_equal(got, want_k)
+
+
+def test_cfg4_sf10_crpq(ldbc):
+    g, G = ldbc
+    sports = g.meta["sports"]
+    base, cnt = g.meta["base"], g.meta["count"]
+    r = R.crpq(G, ["m", "t", "u", "p"], [("m", "hasTag", "t"), ("m", "hasCreator", "u"), ("m", "replyOf*", "p")],
+               var_label={"p": "Post"}, var_const={"t": sports})
+    rows = r.rows()
+    tagged = np.unique(g.src[(g.label == g.label_names.index("hasTag")) & (g.dst == sports)])
+    # closed form: one creator and one root post per message -> one tuple each
+    assert rows.shape == (tagged.size, 4)
+    assert np.array_equal(rows[:, 0], tagged)          # lexicographic order, m first
+    assert np.all(rows[:, 1] == sports)
+    # sampled tuples against O1 relations of each atom
+    og = oracle.OracleGraph(g)
+    idx = synth.sample_sources(rows.shape[0], 64, seed=4)
+    ms = rows[idx, 0].astype(np.uint32)
+    for col, rx in [(2, "hasCreator"), (3, "replyOf*")]:
+        o = oracle.eval_sources(og, rx, ms)
+        for i, m in enumerate(ms):
+            tgt = o["dst"][o["src"] == m]
+            if rx == "replyOf*":          # p must carry vertex label Post
+                tgt = tgt[(tgt >= base["Post"]) & (tgt < base["Post"] + cnt["Post"])]
+            assert tgt.tolist() == [int(rows[idx[i], col])], (rx, int(m))
+
+
+def test_cfg5_rmat24_sampled():
+    g = synth.rmat_graph(24, seed=24)                  # bench.py --workload cfg5
+    G = R.rpq_graph_load(g)
+    rx = "(a|b)*c*"
+    a = R.rpq_compile(G, rx)
+    # bench.py on one GPU: shard 0 of 16, auto batch width (COUNT)
+    rc = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, shard_index=0, shard_count=16)
+    B = rc.stats()["batch_sources"]
+    assert B % 2 == 0
+    srcs, cnts = [], []
+    for sh in (0, 1):       # half-width batches 0 and 1 mod 32 = batches 0 mod 16
+        s, c = R.rpq_eval_allpairs(G, a, mode=R.RPQ_PER_SOURCE, batch_sources=B // 2, shard_index=sh,
+                                   shard_count=32).source_counts()
+        srcs.append(s)
+        cnts.append(c)
+    s = np.concatenate(srcs)
+    c = np.concatenate(cnts)
+    order = np.argsort(s, kind="stable")
+    s, c = s[order], c[order]
+    assert np.all(np.diff(s.astype(np.int64)) > 0)
+    assert int(c.sum()) == rc.count
+    og = oracle.OracleGraph(g)
+    pick = synth.sample_sources(s.size, 48, seed=24)
+    o = oracle.eval_sources(og, rx, s[pick].astype(np.uint32), pairs=False, threads=os.cpu_count() or 1)
+    assert np.array_equal(o["counts"], c[pick])
