@@ -57,13 +57,19 @@ constexpr uint32_t HUB_EDGES = 512;      // edges per hub segment
 constexpr int TILE_V = 1024;             // vertices per extraction tile
 constexpr int NSTAT = 8;
 #ifndef RPQ_LEVEL_MINB
-#define RPQ_LEVEL_MINB 3
+#define RPQ_LEVEL_MINB 5
+#endif
+#ifndef RPQ_HUB_MINB
+#define RPQ_HUB_MINB 4
 #endif
 #ifndef RPQ_SLOTS
 #define RPQ_SLOTS 8
 #endif
 constexpr int SLOTS = RPQ_SLOTS;          // visited-word loads in flight per lane
-constexpr int KGRP = 8;                 // chunks of a row advanced/expanded together
+#ifndef RPQ_KGRP
+#define RPQ_KGRP 8
+#endif
+constexpr int KGRP = RPQ_KGRP;          // chunks of a row advanced/expanded together (<= 8)
 
 struct DevAuto {
     uint32_t nq;
@@ -347,17 +353,19 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
         auto process = [&](const Buf &b, int e0) {
 #pragma unroll
             for (int e = 0; e < E; ++e) {
-                uint32_t newmask = 0;
+                uint32_t lm = 0;   // chunks of this lane with new bits
                 const uint64_t rb = (uint64_t)b.trow[e] * p.nw + colbase;
 #pragma unroll
                 for (int k = 0; k < KC; ++k) {
                     const uint64_t m = (e0 + e < cnt) ? (f[k] & ~b.vis[e][k]) : 0ull;
                     if (m) {
                         red_or64(p.Vis + rb + ckk[k], m);
+                        lm |= 1u << ((bits >> (8 * k)) & 0xffu);
                         if (STATS) st[S_N_RED]++;
                     }
-                    if (live && __ballot_sync(0xffffffffu, m != 0)) newmask |= 1u << ((bits >> (8 * k)) & 0xffu);
                 }
+                // one warp OR (REDUX) instead of a ballot per chunk
+                const uint32_t newmask = live ? __reduce_or_sync(0xffffffffu, lm) : 0u;
                 // a target state without outgoing transitions is never
                 // expanded: its rows only collect result bits, no activity
                 if (lane == 0 && newmask) {
@@ -404,8 +412,13 @@ __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const
                                                const uint32_t *nbr, uint32_t beg, uint32_t end,
                                                const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
                                                unsigned long long *st, bool &act, bool live) {
-    if (nk > 4) expand_edges<8, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
-    else if (nk > 2) expand_edges<4, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+    if constexpr (KGRP > 4) {
+        if (nk > 4) {
+            expand_edges<8, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+            return;
+        }
+    }
+    if (nk > 2) expand_edges<4, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
     else if (nk > 1) expand_edges<2, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
     else expand_edges<1, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
 }
@@ -554,7 +567,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
 
 // Deferred long rows: a warp per HUB_EDGES-edge segment.
 template <bool STATS>
-__global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level_hub(const DevAuto A, const Layout *__restrict__ Sg,
+__global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A, const Layout *__restrict__ Sg,
                                                                    const LevelArgs p) {
     __shared__ Layout S;
     load_layout(S, Sg, A.nq);
@@ -624,7 +637,7 @@ __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layo
     for (uint64_t i = wid; i < nb; i += nwarps) {
         const uint32_t sv = cand[pidx[b0 + i]];
         const uint32_t w = (uint32_t)(i >> 6), c = w / p.cw;
-        uint64_t f[KGRP] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint64_t f[KGRP] = {};
         if (lane == (int)(w - c * p.cw)) f[0] = 1ull << (i & 63);
         const uint64_t bits = c & 31u;
         const uint32_t xw = c >> 5;
@@ -887,19 +900,40 @@ __device__ __forceinline__ uint64_t ans_word(const DevAuto &A, const Layout &S, 
 }
 
 // COUNT: total popcount of Ans over the hull [vlo, vlo + vn) x [0, nw).
+// A warp per vertex row: lanes over the row's words (coalesced), 4 words per
+// lane and final state loaded together so that every warp keeps several
+// sectors in flight (a streaming read of the final states' rows).
 __global__ void k_count_total(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
                               uint32_t nw, unsigned long long *total, const Ctrl *ctrl, uint64_t nunits,
                               int force_dense) {
     if (!force_dense && ctrl && (uint64_t)ctrl->ntouched * 4 <= nunits) return;   // sparse: k_count_touched counts
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
     unsigned long long acc = 0;
-    const uint64_t n = vn * nw;
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t v = vlo + (uint32_t)(i / nw);
-        acc += __popcll(ans_word(A, S, Vis, v, i % nw, nw));
+    for (uint64_t r = wid; r < vn; r += nwarps) {
+        const uint32_t v = vlo + (uint32_t)r;
+        for (uint32_t w0 = 0; w0 < nw; w0 += 128) {
+            uint64_t x[4] = {0, 0, 0, 0};
+            uint64_t fm = A.final_mask;
+            while (fm) {
+                const int q = __ffsll((long long)fm) - 1;
+                fm &= fm - 1;
+                if (v - S.lo[q] >= S.len[q]) continue;
+                const uint64_t *rp = Vis + (S.row_base[q] + (v - S.lo[q])) * nw;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t w = w0 + 32u * j + lane;
+                    if (w < nw) x[j] |= ld_cg(rp + w);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc += __popcll(x[j]);
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(total, acc);
+    if (lane == 0 && acc) atomicAdd(total, acc);
 }
 
 // Per-(source, tile) counts by warp ballot transposes: a warp takes a tile of
@@ -1692,7 +1726,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     std::swap(P1.Xcur, P1.Xnext);
     std::swap(P1.XBcur, P1.XBnext);
     const int lgrid = 148 * RPQ_LEVEL_MINB;   // persistent: warps fetch work units dynamically
-    const int hgrid = 148 * RPQ_LEVEL_MINB;
+    const int hgrid = 148 * RPQ_HUB_MINB;
     LevelGraph LG;
     if (nbatches && !sparse_done && !getenv("RPQ_HOST_LOOP")) {
         cudaError_t ge = stats ? build_level_graph<true>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords)
@@ -1820,7 +1854,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             // COUNT: accumulate on the device (sparse or dense path chosen
             // there from the touched-unit count); no host round trip
             k_count_touched<<<148 * 8, 256, 0, s>>>(A, S, P0, nunits, d_total, dead_final);
-            if (vn) k_count_total<<<grid_for(vn * nw), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, d_total, ctrl,
+            if (vn) k_count_total<<<grid_for(vn * 32), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, d_total, ctrl,
                                                                      nunits, dead_final);
             ST.kernel_launches += vn ? 2 : 1;
             total += eps_np;
