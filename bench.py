@@ -67,10 +67,10 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic():
-    """ncu dram bytes per k_level launch for the default workload, committed
-    under profiles/ (see profiles/README.md); None if absent."""
-    p = os.path.join(ROOT, "profiles", "traffic_cfg2.json")
+def load_traffic(workload):
+    """ncu DRAM bytes per k_level launch for the workload, committed under
+    profiles/ (see profiles/README.md); None if absent."""
+    p = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
     if os.path.exists(p):
         with open(p) as f:
             return json.load(f)
@@ -286,7 +286,7 @@ def run_ours(args):
     step_bytes = probe_bytes * args.steps
     achieved = step_bytes / (agg["expand_ms"] / 1e3) / 1e9 if agg["expand_ms"] > 0 else None
     per_launch = probe_bytes / max(1, probe_levels)
-    traffic = load_traffic()
+    traffic = load_traffic(args.workload)
     line = {
         "metric": "all-pairs RPQ product-edges traversed/s",
         "value": value,
@@ -315,7 +315,11 @@ def run_ours(args):
                      "launches": agg["levels"],
                      "level_loop_ms_per_step": agg["expand_ms"] / args.steps,
                      "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                     "traffic_source": traffic.get("source") if traffic else None},
+                     "traffic_source": traffic.get("source") if traffic else None,
+                     # the same ncu DRAM bytes per launch over this run's average launch
+                     # duration: the measured (not algorithmic) bandwidth of the loop
+                     "traffic_gbs": (traffic["dram_bytes_per_launch"] / (agg["expand_ms"] / 1e3 / agg["levels"]) / 1e9)
+                     if traffic and agg["expand_ms"] > 0 and agg["levels"] else None},
         "e2e": {"value": pe_per_step / (e2e_step / 1e3), "unit": "PE/s", "ms_per_step": e2e_step,
                 "h2d_bytes_per_step": h2d * 1, "d2h_bytes_per_step": 8 * len(queries),
                 "includes": "rpq_graph_load from pinned host arrays + compile + eval + count readback"},

@@ -1,7 +1,7 @@
 """Turn the ncu captures brought back in gpurun_out/ into the committed
 summaries under profiles/ (run here, on the CPU box).
 
-usage: python scripts/make_profiles.py <round tag> <launches.csv> <traffic.csv> <full.ncu-rep>
+usage: python scripts/make_profiles.py <round tag> <dir written by scripts/profile_round.sh>
 """
 import csv, json, os, shutil, subprocess, sys
 
@@ -26,23 +26,7 @@ def summarise(kind, path):
     return json.loads(out)
 
 
-def main():
-    tag, launches, traffic, rep = sys.argv[1:5]
-    pdir = os.path.join(ROOT, "profiles")
-    os.makedirs(pdir, exist_ok=True)
-    L = summarise("launches", launches)
-    with open(os.path.join(pdir, f"{tag}_launches_cfg2.json"), "w") as f:
-        json.dump(L, f, indent=1)
-    shutil.copy(launches, os.path.join(pdir, f"{tag}_launches_cfg2.csv"))
-    T = summarise("traffic", traffic)
-    k = T["k_level"]
-    with open(os.path.join(pdir, "traffic_cfg2.json"), "w") as f:
-        json.dump({"kernel": "k_level", "dram_bytes_per_launch": k["dram_bytes_per_launch"],
-                   "launches": k["launches"], "round": tag,
-                   "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-                             "-k regex:k_level over one COUNT evaluation of each cfg2 query "
-                             "(scripts/prof_cfg2.py, RPQ_HOST_LOOP=1, PROF_NOSTATS=1)",
-                   "all": T}, f, indent=1)
+def full_summary(rep, out_txt):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     h, u = rows[0], rows[1]
@@ -53,10 +37,39 @@ def main():
         for i, n in enumerate(h):
             if n in KEYS:
                 lines.append(f"  {n:60s} {row[i]:>20s} {u[i]}")
-    with open(os.path.join(pdir, f"{tag}_k_level_full.txt"), "w") as f:
+    with open(out_txt, "w") as f:
         f.write("\n".join(lines) + "\n")
-    shutil.copy(rep, os.path.join(pdir, f"{tag}_k_level.ncu-rep"))
-    print(open(os.path.join(pdir, f"{tag}_k_level_full.txt")).read())
+    return "\n".join(lines)
+
+
+def main():
+    """usage: make_profiles.py TAG DIR -- DIR holds the outputs of
+    scripts/profile_round.sh (launches_cfg2.csv, traffic_<wl>.csv,
+    full_<wl>.ncu-rep)."""
+    tag, d = sys.argv[1], sys.argv[2]
+    pdir = os.path.join(ROOT, "profiles")
+    os.makedirs(pdir, exist_ok=True)
+    L = summarise("launches", os.path.join(d, "launches_cfg2.csv"))
+    with open(os.path.join(pdir, f"{tag}_launches_cfg2.json"), "w") as f:
+        json.dump(L, f, indent=1)
+    shutil.copy(os.path.join(d, "launches_cfg2.csv"), os.path.join(pdir, f"{tag}_launches_cfg2.csv"))
+    for fn in sorted(os.listdir(d)):
+        if fn.startswith("traffic_") and fn.endswith(".csv"):
+            wl = fn[len("traffic_"):-4]
+            T = summarise("traffic", os.path.join(d, fn))
+            k = T["k_level"]
+            shards = " 64" if wl == "cfg5" else ""
+            with open(os.path.join(pdir, f"traffic_{wl}.json"), "w") as f:
+                json.dump({"kernel": "k_level", "dram_bytes_per_launch": k["dram_bytes_per_launch"],
+                           "launches": k["launches"], "round": tag,
+                           "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
+                                     f"-k regex:k_level over one COUNT evaluation of each {wl} query "
+                                     f"(scripts/prof_workload.py {wl}{shards}, RPQ_HOST_LOOP=1, PROF_NOSTATS=1)",
+                           "all": T}, f, indent=1)
+        if fn.startswith("full_") and fn.endswith(".ncu-rep"):
+            wl = fn[len("full_"):-len(".ncu-rep")]
+            print(full_summary(os.path.join(d, fn), os.path.join(pdir, f"{tag}_k_level_full_{wl}.txt")))
+            shutil.copy(os.path.join(d, fn), os.path.join(pdir, f"{tag}_k_level_{wl}.ncu-rep"))
 
 
 if __name__ == "__main__":
