@@ -147,9 +147,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # BENCH_SINGLE_GPU_TEST=1 (testing aid only): every rank on cuda:0 over
+    # gloo, to exercise the N>1 code path on a one-GPU box
+    one_gpu_test = os.environ.get("BENCH_SINGLE_GPU_TEST") == "1"
+    if one_gpu_test:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu_test:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if one_gpu_test else "cuda"   # device of the reduced scalars
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     wl = WORKLOADS[args.workload]
@@ -236,10 +245,10 @@ def run_ours(args):
     total_ms = float(sum(times))
     pe_total = probe_pe * args.steps          # PE is a property of (graph, query, shard)
     if world > 1:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
-        pt = torch.tensor([float(pe_total), float(agg["count"])], dtype=torch.float64, device="cuda")
+        pt = torch.tensor([float(pe_total), float(agg["count"])], dtype=torch.float64, device=red_dev)
         dist.all_reduce(pt, op=dist.ReduceOp.SUM)
         pe_total, count_total = int(pt[0].item()), int(pt[1].item())
     else:
@@ -272,7 +281,7 @@ def run_ours(args):
             e2e_ms.append(dt)
     e2e_step = statistics.median(e2e_ms)
     if world > 1:
-        tt = torch.tensor([e2e_step], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([e2e_step], dtype=torch.float64, device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_step = float(tt.item())
 
