@@ -694,8 +694,9 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_sparse(const DevAuto A, const
                                                           unsigned long long *stats,
                                                           const unsigned long long *start = nullptr,
                                                           uint32_t *osrc = nullptr, uint32_t *odst = nullptr,
-                                                          int *err = nullptr) {
+                                                          int *err = nullptr, const uint64_t *n_dev = nullptr) {
     __shared__ uint64_t tab_s[SP_WARPS][SP_H];
+    if (n_dev) n = *n_dev;
     __shared__ uint64_t que_s[SP_WARPS][SP_Q];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     uint64_t *tab = tab_s[wl], *que = que_s[wl];
@@ -788,6 +789,112 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_sparse(const DevAuto A, const
     if (STATS && !WRITE && lane == 0) {
         if (pe_acc) atomicAdd(stats + S_PE, pe_acc);
         if (src_done) atomicAdd(stats + S_ITEMS, src_done);
+    }
+}
+
+// Thread tier of the sparse engine: one thread per source, its visited
+// (vertex, state) keys in a list of ST_K entries that is also the BFS FIFO
+// (keys are appended in discovery order and expanded in that order).  Meant
+// for reach sets of a handful of product vertices (replyOf* ancestor chains:
+// depth ~2); a source that discovers more than ST_K keys or scans more than
+// ST_EMAX edges is flagged (tovf) and goes to the warp tier (k_sparse).
+// Distinct final targets are the distinct vertices of keys in final states.
+constexpr int ST_K = 32;
+constexpr uint32_t ST_EMAX = 256;
+
+template <bool STATS, bool WRITE>
+__global__ void __launch_bounds__(256) k_sparse_thread(const DevAuto A, const uint32_t *__restrict__ cand,
+                                                       const uint32_t *__restrict__ pidx, uint64_t n, uint64_t B,
+                                                       uint32_t shard_index, uint32_t shard_count,
+                                                       unsigned long long *counts, uint8_t *tovf,
+                                                       unsigned long long *stats,
+                                                       const unsigned long long *start = nullptr,
+                                                       uint32_t *osrc = nullptr, uint32_t *odst = nullptr) {
+    uint64_t lst[ST_K];
+    unsigned long long pe_acc = 0, src_done = 0;
+    for (uint64_t pi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pi < n;
+         pi += (uint64_t)gridDim.x * blockDim.x) {
+        if ((pi / B) % shard_count != shard_index) continue;
+        if (WRITE && tovf[pi]) continue;
+        const uint32_t s = cand[pidx[pi]];
+        int nl = 1;
+        lst[0] = (uint64_t)s << 8;
+        bool ovf = false;
+        uint32_t scanned = 0;
+        for (int h = 0; h < nl && !ovf; ++h) {
+            const uint32_t v = (uint32_t)(lst[h] >> 8), q = (uint32_t)(lst[h] & 0xff);
+            for (int t = A.toff[q]; t < A.toff[q + 1] && !ovf; ++t) {
+                const uint32_t q2 = A.tto[t];
+                const uint32_t *off = A.off[A.tslot[t]];
+                const uint32_t beg = __ldg(off + v), end = __ldg(off + v + 1);
+                scanned += end - beg;
+                if (scanned > ST_EMAX) { ovf = true; break; }
+                const uint32_t *nbr = A.nbr[A.tslot[t]];
+                for (uint32_t j = beg; j < end; ++j) {
+                    const uint64_t key = ((uint64_t)__ldg(nbr + j) << 8) | q2;
+                    bool found = false;
+                    for (int i = 0; i < nl && !found; ++i) found = lst[i] == key;
+                    if (found) continue;
+                    if (nl == ST_K) { ovf = true; break; }
+                    lst[nl++] = key;
+                }
+            }
+        }
+        if (ovf) {
+            if (!WRITE) { tovf[pi] = 1; counts[pi] = 0; }
+            continue;
+        }
+        // distinct vertices among keys in final states (first occurrences)
+        unsigned long long cnt = 0;
+        for (int i = 0; i < nl; ++i) {
+            const uint32_t vi = (uint32_t)(lst[i] >> 8);
+            if (!((A.final_mask >> (lst[i] & 0xff)) & 1ull)) continue;
+            bool dup = false;
+            for (int j = 0; j < i && !dup; ++j)
+                dup = ((A.final_mask >> (lst[j] & 0xff)) & 1ull) && (uint32_t)(lst[j] >> 8) == vi;
+            if (dup) continue;
+            if constexpr (WRITE) {
+                // rank among the distinct final vertices -> sorted output
+                unsigned long long r = 0;
+                for (int j = 0; j < nl; ++j) {
+                    const uint32_t vj = (uint32_t)(lst[j] >> 8);
+                    if (!((A.final_mask >> (lst[j] & 0xff)) & 1ull) || vj >= vi) continue;
+                    bool dj = false;   // count each smaller vertex once
+                    for (int k = 0; k < j && !dj; ++k)
+                        dj = ((A.final_mask >> (lst[k] & 0xff)) & 1ull) && (uint32_t)(lst[k] >> 8) == vj;
+                    r += !dj;
+                }
+                const unsigned long long o = start[pidx[pi]] + r;
+                osrc[o] = s;
+                odst[o] = vi;
+            }
+            ++cnt;
+        }
+        if (!WRITE) {
+            counts[pi] = cnt;
+            if (STATS) {
+                pe_acc += scanned;   // every key was expanded: the product edges of the reach (PE, R12)
+                src_done++;
+            }
+        }
+    }
+    if (STATS && !WRITE) {
+        if (pe_acc) atomicAdd(stats + S_PE, pe_acc);
+        if (src_done) atomicAdd(stats + S_ITEMS, src_done);
+    }
+}
+
+__global__ void k_sum_flags(const uint8_t *flag, const uint32_t *idx, uint64_t n, unsigned long long *out) {
+    unsigned long long c = 0;
+    for (uint64_t k = threadIdx.x; k < n; k += blockDim.x) c += flag[idx[k]];
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    __shared__ unsigned long long w[32];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += w[i];
+        *out = t;
     }
 }
 
@@ -1460,8 +1567,12 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         const bool force_sparse = eng && !strcmp(eng, "sparse");
         if (np && !force_dense) {
             unsigned long long *sc = (unsigned long long *)ws.get(np * 8);
-            uint8_t *sov = (uint8_t *)ws.get(np);
-            if (!sc || !sov) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sparse)"));
+            uint8_t *sov = (uint8_t *)ws.get(np);            // warp tier overflowed -> dense engine
+            uint8_t *tov = (uint8_t *)ws.get(np);            // thread tier overflowed -> warp tier
+            uint32_t *tlist = (uint32_t *)ws.get(np * 4);    // ... their productive indices
+            uint64_t *d_nt = (uint64_t *)ws.get(8);
+            if (!sc || !sov || !tov || !tlist || !d_nt)
+                return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sparse)"));
             bool use = force_sparse;
             if (!use) {
                 const uint64_t ns = std::min<uint64_t>(np, 2048);
@@ -1472,15 +1583,15 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                 RPQ_CUDA_TRY(cudaMemcpyAsync(didx, hidx.data(), ns * 4, cudaMemcpyHostToDevice, s));
                 k_sparse<false, false><<<grid_for(ns * 32, SP_WARPS * 32, 148 * 8), SP_WARPS * 32, 0, s>>>(
                     A, cand, pidx, didx, ns, B, 0, 1, sc, sov, d_stats);
-                ST.kernel_launches++;
-                std::vector<uint8_t> hov(np);
-                // flags of the sampled indices only
-                std::vector<uint8_t> all(np);
-                RPQ_CUDA_TRY(cudaMemcpyAsync(all.data(), sov, np, cudaMemcpyDeviceToHost, s));
+                // overflow flags of the sampled indices, summed on the device
+                unsigned long long *d_nov = (unsigned long long *)ws.get(8);
+                if (!d_nov) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                k_sum_flags<<<1, 256, 0, s>>>(sov, didx, ns, d_nov);
+                ST.kernel_launches += 2;
+                unsigned long long nov = 0;
+                RPQ_CUDA_TRY(cudaMemcpyAsync(&nov, d_nov, 8, cudaMemcpyDeviceToHost, s));
                 RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-                uint64_t nov = 0;
                 HM("sparse sample");
-                for (uint64_t k = 0; k < ns; ++k) nov += all[hidx[k]];
                 use = nov * 50 <= ns;   // <= 2 % of the sample overflows
             }
             if (use) {
@@ -1489,13 +1600,32 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                 RPQ_CUDA_TRY(cudaMemsetAsync(sov, 0, np, s));
                 cudaEvent_t sp0 = nullptr, sp1 = nullptr;
                 if (timeit) { cudaEventCreate(&sp0); cudaEventCreate(&sp1); cudaEventRecord(sp0, s); }
+                // thread tier over every source of the shard, then the warp
+                // tier over the sources the thread tier could not hold
+                RPQ_CUDA_TRY(cudaMemsetAsync(tov, 0, np, s));
                 if (stats)
-                    k_sparse<true, false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B, o.shard_index,
-                                                                     shard_count, sc, sov, d_stats);
+                    k_sparse_thread<true, false><<<grid_for(np), 256, 0, s>>>(A, cand, pidx, np, B, o.shard_index,
+                                                                             shard_count, sc, tov, d_stats);
                 else
-                    k_sparse<false, false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B, o.shard_index,
-                                                                      shard_count, sc, sov, d_stats);
-                ST.kernel_launches++;
+                    k_sparse_thread<false, false><<<grid_for(np), 256, 0, s>>>(A, cand, pidx, np, B, o.shard_index,
+                                                                              shard_count, sc, tov, d_stats);
+                {
+                    size_t tt = 0;
+                    thrust::counting_iterator<uint32_t> itt(0);
+                    cub::DeviceSelect::Flagged(nullptr, tt, itt, tov, tlist, d_nt, (int64_t)np, s);
+                    void *tmpt = ws.get(tt);
+                    if (!tmpt) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                    cub::DeviceSelect::Flagged(tmpt, tt, itt, tov, tlist, d_nt, (int64_t)np, s);
+                }
+                if (stats)
+                    k_sparse<true, false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, tlist, np, B, o.shard_index,
+                                                                     shard_count, sc, sov, d_stats, nullptr, nullptr,
+                                                                     nullptr, nullptr, d_nt);
+                else
+                    k_sparse<false, false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, tlist, np, B, o.shard_index,
+                                                                      shard_count, sc, sov, d_stats, nullptr, nullptr,
+                                                                      nullptr, nullptr, d_nt);
+                ST.kernel_launches += 3;
                 if (timeit) {
                     cudaEventRecord(sp1, s);
                     cudaEventSynchronize(sp1);
@@ -1599,11 +1729,14 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                         rpq_result_release(sub_keep);
                         return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (%llu pairs)", (unsigned long long)tot));
                     }
-                    k_sparse<false, true><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, nullptr, np, B,
+                    k_sparse_thread<false, true><<<grid_for(np), 256, 0, s>>>(A, cand, pidx, np, B, o.shard_index,
+                                                                             shard_count, sc, tov, d_stats, start,
+                                                                             res->cols[0], res->cols[1]);
+                    k_sparse<false, true><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, tlist, np, B,
                                                                             o.shard_index, shard_count, sc, sov,
                                                                             d_stats, start, res->cols[0],
-                                                                            res->cols[1], d_err);
-                    ST.kernel_launches++;
+                                                                            res->cols[1], d_err, d_nt);
+                    ST.kernel_launches += 2;
                     if (sub_keep && sub_keep->n_ps) {
                         unsigned long long *ss = (unsigned long long *)ws.get(sub_keep->n_ps * 8);
                         size_t tb3 = 0;
