@@ -234,6 +234,14 @@ const char *rpq_last_error(void);
 rpq_status rpq_device_count(int *n);
 /* library build string (arch, version) */
 const char *rpq_version(void);
+/* Device memory: per-batch state arrays and result buffers (pairs, CRPQ
+ * tuples, per-source counts) come from the device's stream-ordered memory
+ * pool, which keeps freed blocks reserved so that repeated evaluations do not
+ * pay for page mapping (cudaMalloc of a 64 GB pair buffer took 26 ms on a
+ * B200).  rpq_trim_memory returns the reserved but unused bytes of `device`'s
+ * pool to the driver (e.g. before handing HBM to another allocator).
+ * RPQ_EINVAL if device is not a CUDA device; RPQ_ECUDA on driver errors. */
+rpq_status rpq_trim_memory(int device);
 
 #ifdef __cplusplus
 }

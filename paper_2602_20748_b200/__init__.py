@@ -108,7 +108,7 @@ EXPORTED = [
     "rpq_nfa_accepts", "rpq_eval_allpairs", "rpq_eval_single_source", "rpq_eval_sources",
     "crpq_eval", "rpq_result_count", "rpq_result_device_view", "rpq_result_copy_host",
     "rpq_result_source_counts", "rpq_result_stats", "rpq_result_free", "rpq_last_error",
-    "rpq_device_count", "rpq_version", "rpq_shard_plan",
+    "rpq_device_count", "rpq_version", "rpq_shard_plan", "rpq_trim_memory",
 ]
 
 _c = {}
@@ -140,6 +140,7 @@ _c["rpq_result_free"] = _proto("rpq_result_free", None, [_vp])
 _c["rpq_last_error"] = _proto("rpq_last_error", ctypes.c_char_p, [])
 _c["rpq_device_count"] = _proto("rpq_device_count", _st, [_P(ctypes.c_int)])
 _c["rpq_version"] = _proto("rpq_version", ctypes.c_char_p, [])
+_c["rpq_trim_memory"] = _proto("rpq_trim_memory", _st, [ctypes.c_int])
 _c["rpq_shard_plan"] = _proto("rpq_shard_plan", _st, [c_u32p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                                       ctypes.c_uint32, c_u32p])
 
@@ -273,6 +274,11 @@ def rpq_device_count() -> int:
 
 def rpq_version() -> str:
     return _c["rpq_version"]().decode()
+
+
+def rpq_trim_memory(device: int = 0) -> None:
+    """Return the library's cached (pooled, unused) device memory to the driver."""
+    _check(_c["rpq_trim_memory"](device))
 
 
 def rpq_shard_plan(productive_idx, num_candidates: int, batch_sources: int, shard_count: int) -> np.ndarray:

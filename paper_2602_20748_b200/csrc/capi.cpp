@@ -110,6 +110,20 @@ void dev_available_invalidate() {
     }
 }
 
+extern "C" rpq_status rpq_trim_memory(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) {
+        cudaGetLastError();
+        return rpq_fail(RPQ_EINVAL, "rpq_trim_memory: no CUDA device %d", device);
+    }
+    cudaMemPool_t pool;
+    RPQ_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+    RPQ_CUDA_TRY(cudaDeviceSynchronize());
+    RPQ_CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
+    dev_available_invalidate();
+    return RPQ_OK;
+}
+
 void dev_free(void *p, void *stream) {
     if (p) cudaFreeAsync(p, (cudaStream_t)stream);
 }
@@ -181,9 +195,11 @@ void rpq_result_release(rpq_result *r) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(r->device);
-    for (uint32_t c = 0; c < RPQ_MAX_COLS; ++c) if (r->cols[c]) cudaFree(r->cols[c]);
-    if (r->ps_src) cudaFree(r->ps_src);
-    if (r->ps_cnt) cudaFree(r->ps_cnt);
+    // result buffers come from the stream-ordered pool (dev_alloc): freed
+    // back to it, ordered on the legacy default stream
+    for (uint32_t c = 0; c < RPQ_MAX_COLS; ++c) if (r->cols[c]) dev_free(r->cols[c], nullptr);
+    if (r->ps_src) dev_free(r->ps_src, nullptr);
+    if (r->ps_cnt) dev_free(r->ps_cnt, nullptr);
     cudaSetDevice(prev);
     delete r;
 }

@@ -436,7 +436,7 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
     res->count = T.n;
     auto fail = [&](rpq_status st) { rpq_result_release(res); return st; };
     for (uint32_t v = 0; v < nvars; ++v) {
-        if (cudaMalloc(&res->cols[v], std::max<uint64_t>(T.n, 1) * 4) != cudaSuccess) {
+        if (!dev_alloc_to(res->cols[v], std::max<uint64_t>(T.n, 1) * 4, s)) {
             cudaGetLastError();
             return fail(rpq_fail(RPQ_ENOMEM, "crpq: out of device memory (result)"));
         }

@@ -1121,62 +1121,68 @@ __global__ void k_fill_eps(unsigned long long *cand_cnt, uint64_t n, unsigned lo
         cand_cnt[j] = val;
 }
 
-// Write sorted (src, dst) pairs: same traversal as k_tile_counts; lane b
-// keeps the running output position of source w*64+b (and +32).
-__global__ void k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
-                              uint32_t nw, uint32_t nb, uint32_t nseg, const uint32_t *cnt_scan,
-                              const uint32_t *cand, const uint32_t *pidx, uint64_t b0,
-                              const unsigned long long *start, uint64_t jlo, uint32_t *osrc, uint32_t *odst) {
-    const int lane = threadIdx.x & 31;
+// Write sorted (src, dst) pairs.  A warp takes one (1024-vertex tile, word)
+// task = 64 sources: (1) ballot transposes give, per source, 32 masks of 32
+// vertices (shared memory); (2) per source, the warp walks its masks in
+// vertex order and stores each block's targets contiguously.  Each source's
+// tile run is contiguous (start + per-tile scan), so every output sector is
+// written whole by one warp at one time (per-bit scattered writes across 256
+// sources kept ~10^6 partial runs open and doubled the DRAM traffic through
+// L2 evictions).
+constexpr int WP_WARPS = 4;
+__global__ void __launch_bounds__(WP_WARPS * 32)
+k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn, uint32_t nw,
+              uint32_t nb, uint32_t nseg, const uint32_t *cnt_scan, const uint32_t *cand, const uint32_t *pidx,
+              uint64_t b0, const unsigned long long *start, uint64_t jlo, uint32_t *osrc, uint32_t *odst) {
+    __shared__ uint32_t masks_s[WP_WARPS][64 * 32];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    uint32_t *masks = masks_s[wl];
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwg = (nw + 3) / 4;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    for (uint64_t task = wid; task < (uint64_t)nseg * nwg; task += nwarps) {
-        const uint32_t seg = (uint32_t)(task / nwg);
-        const uint32_t w0 = (uint32_t)(task % nwg) * 4;
-        unsigned long long pos[8];
-        uint32_t sid[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const uint32_t i = (w0 + k / 2) * 64 + lane + 32 * (k & 1);
-            if (i < nb) {
-                const uint32_t j = pidx[b0 + i];
-                pos[k] = start[j - jlo] + cnt_scan[(uint64_t)i * nseg + seg];
-                sid[k] = cand[j];
-            } else {
-                pos[k] = 0;
-                sid[k] = 0;
-            }
-        }
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint64_t task = wid; task < (uint64_t)nseg * nw; task += nwarps) {
+        const uint32_t seg = (uint32_t)(task / nw);
+        const uint32_t w = (uint32_t)(task % nw);
         const uint64_t vbeg = (uint64_t)seg * TILE_V, vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
-        for (uint64_t v0 = vbeg; v0 < vend; v0 += 32) {
-            const uint64_t vv = v0 + lane;
-            const uint32_t vid = vlo + (uint32_t)vv;
-            uint64_t x[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                x[k] = (vv < vend && w0 + k < nw) ? ans_word(A, S, Vis, vid, w0 + k, nw) : 0ull;
-            const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (!__ballot_sync(0xffffffffu, x[k] != 0)) continue;
-#pragma unroll 4
-                for (int b = 0; b < 64; ++b) {
-                    const bool has = (x[k] >> b) & 1ull;
-                    const unsigned m = __ballot_sync(0xffffffffu, has);
-                    if (!m) continue;
-                    const int h = b >> 5, bl = b & 31;
-                    const unsigned long long p0 = __shfl_sync(0xffffffffu, pos[2 * k + h], bl);
-                    const uint32_t s = __shfl_sync(0xffffffffu, sid[2 * k + h], bl);
-                    if (has) {
-                        const unsigned long long o = p0 + __popc(m & lt);
-                        osrc[o] = s;
-                        odst[o] = vid;
-                    }
-                    if (lane == bl) pos[2 * k + h] += __popc(m);
+        const int nblk = (int)((vend - vbeg + 31) / 32);
+        // (1) masks[b][blk]: which of the 32 vertices of block blk source b reaches
+        for (int blk = 0; blk < 32; ++blk) {
+            const uint64_t vv = vbeg + (uint64_t)blk * 32 + lane;
+            const uint64_t x = (blk < nblk && vv < vend) ? ans_word(A, S, Vis, vlo + (uint32_t)vv, w, nw) : 0ull;
+            const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+#pragma unroll 8
+            for (int b = 0; b < 32; ++b) {
+                const unsigned m0 = __ballot_sync(0xffffffffu, (lo >> b) & 1u);
+                const unsigned m1 = __ballot_sync(0xffffffffu, (hi >> b) & 1u);
+                if (lane == 0) {
+                    masks[b * 32 + blk] = m0;
+                    masks[(b + 32) * 32 + blk] = m1;
                 }
             }
         }
+        __syncwarp();
+        // (2) per source: walk its 32 block masks in order; each block's
+        // targets go to consecutive positions (a coalesced <= 128 B store),
+        // so the source's tile run is written front to back by this warp
+        for (int b = 0; b < 64; ++b) {
+            const uint32_t i = w * 64 + (uint32_t)b;
+            if (i >= nb) break;
+            const uint32_t j = pidx[b0 + i];
+            unsigned long long o = start[j - jlo] + cnt_scan[(uint64_t)i * nseg + seg];
+            const uint32_t sid = cand[j];
+            const uint32_t vb = vlo + (uint32_t)vbeg + (uint32_t)lane;
+            for (int blk = 0; blk < nblk; ++blk) {
+                const uint32_t m = masks[b * 32 + blk];
+                if (!m) continue;
+                if ((m >> lane) & 1u) {
+                    const unsigned long long q = o + __popc(m & lt);
+                    osrc[q] = sid;
+                    odst[q] = vb + (uint32_t)blk * 32u;
+                }
+                o += __popc(m);
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -1723,8 +1729,8 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                     const uint64_t tot = ls + lc;
                     res->ncols = 2;
                     res->nrows = tot;
-                    if (cudaMalloc(&res->cols[0], std::max<uint64_t>(tot, 1) * 4) != cudaSuccess ||
-                        cudaMalloc(&res->cols[1], std::max<uint64_t>(tot, 1) * 4) != cudaSuccess) {
+                    if (!dev_alloc_to(res->cols[0], std::max<uint64_t>(tot, 1) * 4, s) ||
+                        !dev_alloc_to(res->cols[1], std::max<uint64_t>(tot, 1) * 4, s)) {
                         cudaGetLastError();
                         rpq_result_release(sub_keep);
                         return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (%llu pairs)", (unsigned long long)tot));
@@ -1825,7 +1831,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     }
     struct Block { uint32_t *src, *dst; uint64_t n; };
     std::vector<Block> blocks;
-    struct BlockGuard { std::vector<Block> *b; ~BlockGuard() { for (auto &x : *b) { cudaFree(x.src); cudaFree(x.dst); } } } bgd{&blocks};
+    struct BlockGuard { std::vector<Block> *b; cudaStream_t s; ~BlockGuard() { for (auto &x : *b) { dev_free(x.src, s); dev_free(x.dst, s); } } } bgd{&blocks, s};
 
     uint64_t total = 0;
     // candidate-index interval owned by batch b (non-productive candidates in
@@ -1923,9 +1929,9 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             total += ne;
             if (want_pairs && ne) {
                 Block bl{nullptr, nullptr, ne};
-                if (cudaMalloc(&bl.src, ne * 4) != cudaSuccess || cudaMalloc(&bl.dst, ne * 4) != cudaSuccess) {
+                if (!dev_alloc_to(bl.src, ne * 4, s) || !dev_alloc_to(bl.dst, ne * 4, s)) {
                     cudaGetLastError();
-                    cudaFree(bl.src);
+                    dev_free(bl.src, s);
                     return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (pairs)"));
                 }
                 blocks.push_back(bl);
@@ -2023,15 +2029,17 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         total += bt;
         if (want_pairs && bt) {
             Block bl{nullptr, nullptr, bt};
-            if (cudaMalloc(&bl.src, bt * 4) != cudaSuccess || cudaMalloc(&bl.dst, bt * 4) != cudaSuccess) {
+            HM("pairs: count + scan");
+            if (!dev_alloc_to(bl.src, bt * 4, s) || !dev_alloc_to(bl.dst, bt * 4, s)) {
                 cudaGetLastError();
-                cudaFree(bl.src);
+                dev_free(bl.src, s);
                 return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (%llu pairs)", (unsigned long long)bt));
             }
             blocks.push_back(bl);
+            HM("pairs: cudaMalloc of the block");
             if (vn) {
-                k_write_pairs<<<grid_for(tasks * 32), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, nb, nseg, cnt,
-                                                                   cand, pidx, b0, start, jlo, bl.src, bl.dst);
+                k_write_pairs<<<grid_for((uint64_t)nseg * nw * 32, WP_WARPS * 32, 148 * 16), WP_WARPS * 32, 0, s>>>(
+                    A, S, Vis, vlo, vn, (uint32_t)nw, nb, nseg, cnt, cand, pidx, b0, start, jlo, bl.src, bl.dst);
                 ST.kernel_launches++;
             }
             if (eps) {
@@ -2067,8 +2075,8 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             res->cols[1] = blocks[0].dst;
             blocks.clear();
         } else {
-            if (cudaMalloc(&res->cols[0], std::max<uint64_t>(total, 1) * 4) != cudaSuccess ||
-                cudaMalloc(&res->cols[1], std::max<uint64_t>(total, 1) * 4) != cudaSuccess) {
+            if (!dev_alloc_to(res->cols[0], std::max<uint64_t>(total, 1) * 4, s) ||
+                !dev_alloc_to(res->cols[1], std::max<uint64_t>(total, 1) * 4, s)) {
                 cudaGetLastError();
                 return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (pairs)"));
             }
@@ -2092,7 +2100,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         uint8_t *nz = (uint8_t *)ws.get(nsrc);
         uint64_t *d_n = (uint64_t *)ws.get(8);
         if (!nz || !d_n) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
-        if (cudaMalloc(&res->ps_src, nsrc * 4) != cudaSuccess || cudaMalloc(&res->ps_cnt, nsrc * 8) != cudaSuccess) {
+        if (!dev_alloc_to(res->ps_src, nsrc * 4, s) || !dev_alloc_to(res->ps_cnt, nsrc * 8, s)) {
             cudaGetLastError();
             return fail(rpq_fail(RPQ_ENOMEM, "oom"));
         }

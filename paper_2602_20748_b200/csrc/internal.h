@@ -62,6 +62,11 @@ struct rpq_result {
 // ---- device memory (stream-ordered pool allocator) -----------------------
 void *dev_alloc(size_t bytes, void *stream);          // nullptr on failure
 void dev_free(void *p, void *stream);
+template <class T>
+inline bool dev_alloc_to(T *&p, size_t bytes, void *stream) {
+    p = static_cast<T *>(dev_alloc(bytes, stream));
+    return p != nullptr;
+}
 uint64_t dev_available(bool *cached = nullptr);       // free + pool-reserved-unused bytes (cached)
 void dev_available_invalidate();
 void rpq_result_release(rpq_result *r);

@@ -50,6 +50,15 @@ def test_no_gpu_graph_load_fails_loudly():
     assert e.value.status == R.RPQ_ECUDA
 
 
+def test_no_gpu_trim_memory_einval():
+    import paper_2602_20748_b200 as R
+    if R.rpq_device_count() > 0:
+        pytest.skip("GPU present")
+    with pytest.raises(R.RPQError) as e:
+        R.rpq_trim_memory(0)
+    assert e.value.status == R.RPQ_EINVAL
+
+
 NAMES = ["a", "b", "c", "d", "knows", "replyOf"]
 REGEXES = ["abc*", "abcd", "a*", "knows+", "(a|b)*c", "(a|b)*c*", "ab*c", "a b* c", "a?b*",
            "ab*", "(a|b)b*", "a*b*", "ab*c*", "(a|b|c)*", "(ab)*", "a(b|c)?", "((a|b)c)+",
