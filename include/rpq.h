@@ -65,9 +65,15 @@ typedef struct {
     uint32_t num_vertex_labels;
     const char *const *vertex_label_names;  /* [num_vertex_labels] or NULL */
     int device;                             /* CUDA device ordinal */
-    uint32_t flags;                         /* reserved, 0 */
+    uint32_t flags;                         /* 0 or RPQ_GRAPH_IN_EDGES */
     void *cuda_stream;                      /* cudaStream_t used for the build, NULL = default */
 } rpq_graph_desc;
+
+/* Also build the per-label in-edge CSR (the transposed graph).  LGF keeps
+ * in-edge slices for reverse traversal; here they serve
+ * rpq_eval_targets and CRPQ atoms whose target side is bound (WavePlan's
+ * reverse plans).  Doubles the graph's device memory. */
+#define RPQ_GRAPH_IN_EDGES 1u
 
 /* Copies the host arrays to the device and builds the per-label CSR.
  * Errors: EINVAL (id >= num_vertices, label >= num_labels, NULL arrays with
@@ -115,6 +121,14 @@ rpq_status rpq_nfa_transitions(const rpq_nfa *a, uint32_t *from, uint32_t *label
                                uint32_t cap, uint32_t *n, uint64_t *final_mask);
 /* word membership (host simulation; used to pin the compiler) */
 rpq_status rpq_nfa_accepts(const rpq_nfa *a, const uint32_t *word, uint32_t len, int *accepted);
+/* Automaton of the reversed language L(rho)^R = { w_k ... w_1 : w_1 ... w_k
+ * in L(rho) } (reverse every transition, the old finals become initial, the
+ * old initial state final), then subset construction, minimisation, trim and
+ * canonical numbering as in rpq_compile.  (x, y) in R(rho) on G  <=>
+ * (y, x) in R(rho^R) on the transposed graph: the basis of single-target
+ * evaluation ("single-source" mirrored; reverse plans P:867).
+ * Host-side.  Errors: EINVAL (NULL), EUNSUPPORTED (> RPQ_MAX_STATES). */
+rpq_status rpq_nfa_reverse(const rpq_nfa *a, rpq_nfa **out);
 
 /* ------------------------------------------------------------------------
  * Evaluation (Definition 1): R(rho) = distinct (x, y) such that a
@@ -154,6 +168,18 @@ rpq_status rpq_eval_single_source(const rpq_graph *g, const rpq_nfa *a, uint32_t
  * Pairs are sorted by (src, dst) regardless of input order. */
 rpq_status rpq_eval_sources(const rpq_graph *g, const rpq_nfa *a, const uint32_t *srcs,
                             uint64_t n, const rpq_eval_opts *opts, rpq_result **out);
+/* A set of TARGETS (host array, any order, no duplicates -> else EINVAL):
+ * the pairs (x, t) of R(rho) with t in targets and x in V, evaluated
+ * backwards -- rpq_nfa_reverse(a) traversed over the in-edge CSR from the
+ * targets (the graph must have been loaded with RPQ_GRAPH_IN_EDGES, else
+ * EUNSUPPORTED).  Result columns are (x, t) as for the forward calls, but
+ * rows are sorted by (t, x) (grouped by target); RPQ_PER_SOURCE gives
+ * per-TARGET counts.  epsilon in L(rho) => (t, t) for every target. */
+rpq_status rpq_eval_targets(const rpq_graph *g, const rpq_nfa *a, const uint32_t *targets,
+                            uint64_t n, const rpq_eval_opts *opts, rpq_result **out);
+/* Single target t: { (x, t) }, sorted by x.  t >= |V| -> EINVAL. */
+rpq_status rpq_eval_single_target(const rpq_graph *g, const rpq_nfa *a, uint32_t t,
+                                  const rpq_eval_opts *opts, rpq_result **out);
 
 /* ------------------------------------------------------------------------
  * CRPQ (Definition 2): all homomorphisms f: V_q -> V with

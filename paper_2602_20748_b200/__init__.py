@@ -32,6 +32,7 @@ RPQ_ENOMEM, RPQ_ECUDA, RPQ_ECAPACITY, RPQ_EUNSUPPORTED = -4, -5, -6, -7
 RPQ_SYNTAX_PAPER, RPQ_NO_MINIMIZE = 1, 2
 RPQ_MAX_STATES, RPQ_MAX_TRANSITIONS, RPQ_MAX_QUERY_LABELS = 64, 256, 32
 RPQ_COUNT, RPQ_PAIRS, RPQ_PER_SOURCE, RPQ_STATS, RPQ_TIME_KERNELS = 1, 2, 4, 8, 16
+RPQ_GRAPH_IN_EDGES = 1
 RPQ_MAX_COLS = 16
 
 _STATUS_NAMES = {0: "RPQ_OK", -1: "RPQ_EINVAL", -2: "RPQ_ESYNTAX", -3: "RPQ_ELABEL",
@@ -109,6 +110,7 @@ EXPORTED = [
     "crpq_eval", "rpq_result_count", "rpq_result_device_view", "rpq_result_copy_host",
     "rpq_result_source_counts", "rpq_result_stats", "rpq_result_free", "rpq_last_error",
     "rpq_device_count", "rpq_version", "rpq_shard_plan", "rpq_trim_memory",
+    "rpq_nfa_reverse", "rpq_eval_targets", "rpq_eval_single_target",
 ]
 
 _c = {}
@@ -124,8 +126,13 @@ _c["rpq_nfa_info"] = _proto("rpq_nfa_info", _st, [_vp, c_u32p, c_u32p, c_u32p, _
 _c["rpq_nfa_transitions"] = _proto("rpq_nfa_transitions", _st, [_vp, c_u32p, c_u32p, c_u32p, ctypes.c_uint32,
                                                                 c_u32p, c_u64p])
 _c["rpq_nfa_accepts"] = _proto("rpq_nfa_accepts", _st, [_vp, c_u32p, ctypes.c_uint32, _P(ctypes.c_int)])
+_c["rpq_nfa_reverse"] = _proto("rpq_nfa_reverse", _st, [_vp, _P(_vp)])
 _c["rpq_eval_allpairs"] = _proto("rpq_eval_allpairs", _st, [_vp, _vp, _P(rpq_eval_opts), _P(_vp)])
 _c["rpq_eval_single_source"] = _proto("rpq_eval_single_source", _st, [_vp, _vp, ctypes.c_uint32,
+                                                                      _P(rpq_eval_opts), _P(_vp)])
+_c["rpq_eval_targets"] = _proto("rpq_eval_targets", _st, [_vp, _vp, c_u32p, ctypes.c_uint64,
+                                                          _P(rpq_eval_opts), _P(_vp)])
+_c["rpq_eval_single_target"] = _proto("rpq_eval_single_target", _st, [_vp, _vp, ctypes.c_uint32,
                                                                       _P(rpq_eval_opts), _P(_vp)])
 _c["rpq_eval_sources"] = _proto("rpq_eval_sources", _st, [_vp, _vp, c_u32p, ctypes.c_uint64,
                                                           _P(rpq_eval_opts), _P(_vp)])
@@ -295,9 +302,11 @@ def rpq_last_error() -> str:
 
 
 def rpq_graph_load(graph=None, *, num_vertices=None, src=None, dst=None, label=None, label_names=None,
-                   vertex_label=None, vertex_label_names=None, device: int = 0, stream=None) -> Graph:
+                   vertex_label=None, vertex_label_names=None, device: int = 0, stream=None,
+                   in_edges: bool = False) -> Graph:
     """Load a graph (anything with num_vertices/src/dst/label/label_names, or
-    the arrays as keywords) into a per-label device CSR."""
+    the arrays as keywords) into a per-label device CSR (plus the in-edge CSR
+    with in_edges=True: RPQ_GRAPH_IN_EDGES)."""
     if graph is not None:
         num_vertices, src, dst, label = graph.num_vertices, graph.src, graph.dst, graph.label
         label_names = graph.label_names
@@ -324,6 +333,7 @@ def rpq_graph_load(graph=None, *, num_vertices=None, src=None, dst=None, label=N
         d.vertex_label_names = vnames
     d.device = device
     d.cuda_stream = stream
+    d.flags = RPQ_GRAPH_IN_EDGES if in_edges else 0
     h = ctypes.c_void_p()
     _check(_c["rpq_graph_load"](ctypes.byref(d), ctypes.byref(h)))
     return Graph(h.value, label_names, vertex_label_names or [], int(num_vertices))
@@ -346,6 +356,13 @@ def rpq_compile(g: Graph, regex: str, flags: int = 0) -> Nfa:
     off = ctypes.c_size_t()
     st = _c["rpq_compile"](g.h, regex.encode(), flags, ctypes.byref(h), ctypes.byref(off))
     _check(st, off.value)
+    return Nfa(h.value)
+
+
+def rpq_nfa_reverse(a: Nfa) -> Nfa:
+    """Automaton of the reversed language."""
+    h = ctypes.c_void_p()
+    _check(_c["rpq_nfa_reverse"](a.h, ctypes.byref(h)))
     return Nfa(h.value)
 
 
@@ -386,6 +403,24 @@ def rpq_eval_sources(g: Graph, a: Nfa, sources, opts: Optional[rpq_eval_opts] = 
     h = ctypes.c_void_p()
     _check(_c["rpq_eval_sources"](g.h, a.h, _ptr(s, ctypes.c_uint32), len(sources), ctypes.byref(o),
                                   ctypes.byref(h)))
+    return Result(h.value)
+
+
+def rpq_eval_targets(g: Graph, a: Nfa, targets, opts: Optional[rpq_eval_opts] = None, **kw) -> Result:
+    """(x, t) pairs for the given targets (rows sorted by (t, x)); the graph
+    needs in_edges=True."""
+    o = opts if opts is not None else make_opts(**kw)
+    t = _arr(targets if len(targets) else [0], np.uint32)
+    h = ctypes.c_void_p()
+    _check(_c["rpq_eval_targets"](g.h, a.h, _ptr(t, ctypes.c_uint32), len(targets), ctypes.byref(o),
+                                  ctypes.byref(h)))
+    return Result(h.value)
+
+
+def rpq_eval_single_target(g: Graph, a: Nfa, t: int, opts: Optional[rpq_eval_opts] = None, **kw) -> Result:
+    o = opts if opts is not None else make_opts(**kw)
+    h = ctypes.c_void_p()
+    _check(_c["rpq_eval_single_target"](g.h, a.h, int(t), ctypes.byref(o), ctypes.byref(h)))
     return Result(h.value)
 
 

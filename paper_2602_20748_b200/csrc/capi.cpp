@@ -174,6 +174,10 @@ extern "C" rpq_status rpq_nfa_transitions(const rpq_nfa *a, uint32_t *from, uint
     return RPQ_OK;
 }
 
+extern "C" rpq_status rpq_nfa_reverse(const rpq_nfa *a, rpq_nfa **out) {
+    return reverse_automaton(a, out);
+}
+
 extern "C" rpq_status rpq_nfa_accepts(const rpq_nfa *a, const uint32_t *word, uint32_t len,
                                       int *accepted) {
     if (!a || !accepted || (len && !word)) return rpq_fail(RPQ_EINVAL, "NULL argument");

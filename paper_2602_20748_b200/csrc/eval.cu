@@ -1412,9 +1412,15 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         A.tslot[t] = (uint8_t)slot;
         A.tto[t] = (uint8_t)a->to[t];
     }
+    // reserved bit 1 (rpq_eval_targets): traverse the in-edge CSR, i.e. the
+    // transposed graph, with the reversed automaton
+    const bool reverse = (o.reserved & 2u) != 0;
+    if (reverse && g->in_csr.size() != g->csr.size())
+        return fail(rpq_fail(RPQ_EUNSUPPORTED, "graph loaded without RPQ_GRAPH_IN_EDGES"));
+    const std::vector<LabelCSR> &CSR = reverse ? g->in_csr : g->csr;
     for (size_t k = 0; k < slot_label.size(); ++k) {
-        A.off[k] = g->csr[slot_label[k]].off;
-        A.nbr[k] = g->csr[slot_label[k]].nbr;
+        A.off[k] = CSR[slot_label[k]].off;
+        A.nbr[k] = CSR[slot_label[k]].nbr;
     }
 
     // ---- candidate sources and the productive subset P --------------------
@@ -1454,7 +1460,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     // ---- ranges per state (hull of dst ranges of entering labels) ---------
     std::vector<Range> in_range(a->nq, Range{1, 0});
     for (size_t t = 0; t < a->from.size(); ++t) {
-        const LabelCSR &c = g->csr[a->label[t]];
+        const LabelCSR &c = CSR[a->label[t]];
         in_range[a->to[t]] = hull(in_range[a->to[t]], Range{c.dst_min, c.dst_max});
     }
 
@@ -2195,6 +2201,33 @@ extern "C" rpq_status rpq_eval_sources(const rpq_graph *g, const rpq_nfa *a, con
     st = eval_sources_device(g, a, d, n, opts, out);
     dev_free(d, s);
     return st;
+}
+
+extern "C" rpq_status rpq_eval_targets(const rpq_graph *g, const rpq_nfa *a, const uint32_t *targets,
+                                       uint64_t n, const rpq_eval_opts *opts, rpq_result **out) {
+    rpq_status st = check_common(g, a, out);
+    if (st) return st;
+    if (g->in_csr.size() != g->csr.size())
+        return rpq_fail(RPQ_EUNSUPPORTED, "rpq_eval_targets: graph loaded without RPQ_GRAPH_IN_EDGES");
+    rpq_nfa *rev = nullptr;
+    if ((st = reverse_automaton(a, &rev)) != RPQ_OK) return st;
+    struct NfaGuard { rpq_nfa *p; ~NfaGuard() { delete p; } } ng{rev};
+    rpq_eval_opts o{};
+    if (opts) o = *opts;
+    o.reserved |= 2u;
+    // (t, x) pairs of rho^R on the transposed graph, sorted by (t, x)
+    if ((st = rpq_eval_sources(g, rev, targets, n, &o, out)) != RPQ_OK) return st;
+    rpq_result *r = *out;
+    if (r->ncols == 2) std::swap(r->cols[0], r->cols[1]);   // -> (x, t) columns
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_eval_single_target(const rpq_graph *g, const rpq_nfa *a, uint32_t t,
+                                             const rpq_eval_opts *opts, rpq_result **out) {
+    rpq_status st = check_common(g, a, out);
+    if (st) return st;
+    if (t >= g->nv) return rpq_fail(RPQ_EINVAL, "target %u >= |V| = %u", t, g->nv);
+    return rpq_eval_targets(g, a, &t, 1, opts, out);
 }
 
 extern "C" rpq_status rpq_eval_single_source(const rpq_graph *g, const rpq_nfa *a, uint32_t src,

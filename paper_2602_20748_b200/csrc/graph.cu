@@ -76,6 +76,7 @@ extern "C" void rpq_graph_free(rpq_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
     for (auto &c : g->csr) { cudaFree(c.off); cudaFree(c.nbr); }
+    for (auto &c : g->in_csr) { cudaFree(c.off); cudaFree(c.nbr); }
     if (g->vlabel) cudaFree(g->vlabel);
     delete g;
     dev_available_invalidate();
@@ -130,21 +131,29 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
     if (bad) return rpq_fail(RPQ_EINVAL, "rpq_graph_load: vertex id >= num_vertices or label >= num_labels");
     std::vector<unsigned long long> start(nl + 1, 0);
     for (uint32_t l = 0; l < nl; ++l) start[l + 1] = start[l] + cnt[l];
-    RPQ_CUDA_TRY(cudaMemcpyAsync(d_cnt, start.data(), nl * 8ull, cudaMemcpyHostToDevice, s));
-    if (ne) k_scatter<<<grid_for(ne), 256, 0, s>>>(d_src, d_dst, d_lab, ne, d_cnt, keys);
-    RPQ_CUDA_TRY(cudaGetLastError());
-
     rpq_graph *g = new rpq_graph();
     g->device = d->device;
     g->nv = nv;
     for (uint32_t l = 0; l < nl; ++l) g->label_names.emplace_back(d->label_names[l] ? d->label_names[l] : "");
     g->csr.resize(nl);
+    const bool in_edges = (d->flags & RPQ_GRAPH_IN_EDGES) != 0;
+    if (in_edges) g->in_csr.resize(nl);
     int vbits = 1;
     while (vbits < 32 && (1ull << vbits) < nv) ++vbits;
     auto fail = [&](rpq_status st, const char *m) { rpq_graph_free(g); return rpq_fail(st, "rpq_graph_load: %s", m); };
 
+    // pass 0: out-edge CSR (keys u<<32|w); pass 1 (RPQ_GRAPH_IN_EDGES): the
+    // in-edge CSR of the transposed graph (keys w<<32|u), same construction
+    for (int pass = 0; pass < (in_edges ? 2 : 1); ++pass) {
+    RPQ_CUDA_TRY(cudaMemcpyAsync(d_cnt, start.data(), nl * 8ull, cudaMemcpyHostToDevice, s));
+    if (ne) {
+        if (pass == 0) k_scatter<<<grid_for(ne), 256, 0, s>>>(d_src, d_dst, d_lab, ne, d_cnt, keys);
+        else k_scatter<<<grid_for(ne), 256, 0, s>>>(d_dst, d_src, d_lab, ne, d_cnt, keys);
+    }
+    RPQ_CUDA_TRY(cudaGetLastError());
+    std::vector<LabelCSR> &csrs = pass == 0 ? g->csr : g->in_csr;
     for (uint32_t l = 0; l < nl; ++l) {
-        LabelCSR &c = g->csr[l];
+        LabelCSR &c = csrs[l];
         uint64_t n = cnt[l];
         c.off = nullptr;
         if (cudaMalloc(&c.off, (nv + 1ull) * 4) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "CSR offsets"); }
@@ -195,7 +204,8 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
         c.src_max = (uint32_t)(klast >> 32);
         c.dst_min = mm[0];
         c.dst_max = mm[1];
-        g->ne += m;
+        if (pass == 0) g->ne += m;
+    }
     }
     if (d->vertex_label) {
         if (d->num_vertex_labels && d->vertex_label_names)

@@ -29,6 +29,7 @@ struct rpq_graph {
     std::vector<std::string> label_names;
     std::vector<std::string> vlabel_names;
     std::vector<LabelCSR> csr;   // [num_labels]
+    std::vector<LabelCSR> in_csr;   // [num_labels] in-edges (RPQ_GRAPH_IN_EDGES), else empty
     uint16_t *vlabel = nullptr;  // device [nv] or null
     std::vector<uint16_t> h_vlabel;   // host copy (CRPQ planning)
 };
@@ -83,6 +84,7 @@ void batch_plan(const uint32_t *bfirst, uint64_t nbatches, uint64_t nsrc, std::v
 // ---- compile (regex.cpp) -------------------------------------------------
 rpq_status compile_regex(const std::vector<std::string> &vocab, const char *regex, uint32_t flags,
                          rpq_nfa **out, size_t *err_offset);
+rpq_status reverse_automaton(const rpq_nfa *a, rpq_nfa **out);
 
 #define RPQ_CUDA_TRY(expr)                                                              \
     do {                                                                                \

@@ -317,6 +317,37 @@ Auto hopcroft(const Auto &D, const std::vector<int> &alpha) {
     return Q;   // the dead block is removed by trim_canon (not co-reachable)
 }
 
+// Final stage shared by rpq_compile and rpq_nfa_reverse: the trimmed,
+// canonically numbered automaton -> rpq_nfa (limits of the kernels checked).
+rpq_status make_nfa(const Auto &R, bool is_dfa, const std::vector<std::string> &vocab, rpq_nfa **out) {
+    if (R.n > RPQ_MAX_STATES)
+        return rpq_fail(RPQ_EUNSUPPORTED, "rpq_compile: %d automaton states > %d", R.n, RPQ_MAX_STATES);
+    rpq_nfa *a = new rpq_nfa();
+    a->nq = (uint32_t)R.n;
+    a->is_dfa = is_dfa;
+    a->vocab = vocab;
+    a->vocab_size = (uint32_t)vocab.size();
+    a->off.assign(a->nq + 1, 0);
+    std::set<uint32_t> labs;
+    for (int q = 0; q < R.n; ++q) {
+        if (R.fin[q]) a->final_mask |= 1ull << q;
+        for (auto &e : R.out[q]) {
+            a->from.push_back((uint32_t)q);
+            a->label.push_back((uint32_t)e.first);
+            a->to.push_back((uint32_t)e.second);
+            labs.insert((uint32_t)e.first);
+        }
+        a->off[q + 1] = (uint32_t)a->from.size();
+    }
+    a->accepts_empty = R.n > 0 && R.fin[0];
+    if (a->from.size() > RPQ_MAX_TRANSITIONS || labs.size() > RPQ_MAX_QUERY_LABELS) {
+        delete a;
+        return rpq_fail(RPQ_EUNSUPPORTED, "rpq_compile: automaton too large for the kernels");
+    }
+    *out = a;
+    return RPQ_OK;
+}
+
 }  // namespace
 
 rpq_status compile_regex(const std::vector<std::string> &vocab, const char *regex, uint32_t flags,
@@ -369,30 +400,38 @@ rpq_status compile_regex(const std::vector<std::string> &vocab, const char *rege
         if (M.n <= RPQ_MAX_STATES) { R = M; is_dfa = true; }
     }
     if (!is_dfa) R = trim_canon(N);
-    if (R.n > RPQ_MAX_STATES)
-        return rpq_fail(RPQ_EUNSUPPORTED, "rpq_compile: %d automaton states > %d", R.n, RPQ_MAX_STATES);
-    rpq_nfa *a = new rpq_nfa();
-    a->nq = (uint32_t)R.n;
-    a->is_dfa = is_dfa;
-    a->vocab = vocab;
-    a->vocab_size = (uint32_t)vocab.size();
-    a->off.assign(a->nq + 1, 0);
-    std::set<uint32_t> labs;
-    for (int q = 0; q < R.n; ++q) {
-        if (R.fin[q]) a->final_mask |= 1ull << q;
-        for (auto &e : R.out[q]) {
-            a->from.push_back((uint32_t)q);
-            a->label.push_back((uint32_t)e.first);
-            a->to.push_back((uint32_t)e.second);
-            labs.insert((uint32_t)e.first);
-        }
-        a->off[q + 1] = (uint32_t)a->from.size();
+    return make_nfa(R, is_dfa, vocab, out);
+}
+
+// Reversed language (rpq_nfa_reverse): reverse every transition of the
+// epsilon-free automaton, a new initial state 0 takes the reversed
+// transitions into the old final states (so no epsilon moves are needed), the
+// old initial state becomes final (and 0 too when epsilon is accepted); then
+// the same determinise / minimise / trim / number pipeline as rpq_compile.
+rpq_status reverse_automaton(const rpq_nfa *a, rpq_nfa **out) {
+    if (out) *out = nullptr;
+    if (!a || !out) return rpq_fail(RPQ_EINVAL, "rpq_nfa_reverse: NULL argument");
+    Auto N;
+    N.n = (int)a->nq + 1;
+    N.out.resize(N.n);
+    N.fin.assign(N.n, 0);
+    std::vector<int> alpha;
+    for (size_t t = 0; t < a->from.size(); ++t) {
+        const int q = (int)a->from[t], l = (int)a->label[t], q2 = (int)a->to[t];
+        N.out[q2 + 1].push_back({l, q + 1});
+        if ((a->final_mask >> q2) & 1ull) N.out[0].push_back({l, q + 1});
+        alpha.push_back(l);
     }
-    a->accepts_empty = R.n > 0 && R.fin[0];
-    if (a->from.size() > RPQ_MAX_TRANSITIONS || labs.size() > RPQ_MAX_QUERY_LABELS) {
-        delete a;
-        return rpq_fail(RPQ_EUNSUPPORTED, "rpq_compile: automaton too large for the kernels");
+    if (a->nq) N.fin[1] = 1;               // the old initial state
+    N.fin[0] = a->accepts_empty;
+    std::sort(alpha.begin(), alpha.end());
+    alpha.erase(std::unique(alpha.begin(), alpha.end()), alpha.end());
+    Auto R, D;
+    bool is_dfa = false;
+    if (subset(N, alpha, 4096, D)) {
+        Auto M = trim_canon(hopcroft(D, alpha));
+        if (M.n <= RPQ_MAX_STATES) { R = M; is_dfa = true; }
     }
-    *out = a;
-    return RPQ_OK;
+    if (!is_dfa) R = trim_canon(N);
+    return make_nfa(R, is_dfa, a->vocab, out);
 }

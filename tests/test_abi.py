@@ -127,3 +127,29 @@ def test_longest_match_tokenisation():
     import paper_2602_20748_b200 as R
     tr, fin = R.rpq_compile_labels(["reply", "replyOf", "knows"], "replyOf*").transitions()
     assert tr == [(0, 1, 0)] and fin == [0]
+
+
+@pytest.mark.parametrize("rx", ["abc*", "(a|b)*c", "a?b*", "((a|b)c)+", "a(b|c)?", "(ab)*", "a b* c", "c*",
+                                "(a|b)*(c|d)(a|b)*", "a(b|c)*d+"])
+def test_nfa_reverse_language(rx):
+    """rpq_nfa_reverse accepts exactly the reversed words (all words of length
+    <= 6 against Python re on the reversed word), and reversing twice gives
+    back the same canonical minimal DFA."""
+    import paper_2602_20748_b200 as R
+    pat = re.compile(oracle.to_python_re(rx, NAMES[:4]))
+    a = R.rpq_compile_labels(NAMES[:4], rx)
+    r = R.rpq_nfa_reverse(a)
+    assert r.info()["accepts_empty"] == a.info()["accepts_empty"]
+    for n in range(7):
+        for w in itertools.product(range(4), repeat=n):
+            want = bool(pat.fullmatch("".join(chr(0xE000 + x) for x in reversed(w))))
+            assert r.accepts(list(w)) == want, (rx, w)
+    assert R.rpq_nfa_reverse(r).transitions() == a.transitions()
+
+
+def test_nfa_reverse_matches_reversed_regex():
+    """abc* reversed is c*ba; (a|b)*c reversed is c(a|b)*: identical minimal DFAs."""
+    import paper_2602_20748_b200 as R
+    for rx, rrx in [("abc*", "c*ba"), ("(a|b)*c", "c(a|b)*"), ("a b* c", "c b* a")]:
+        assert R.rpq_nfa_reverse(R.rpq_compile_labels(NAMES, rx)).transitions() == \
+            R.rpq_compile_labels(NAMES, rrx).transitions()
