@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cub/cub.cuh>
 #include <thrust/iterator/counting_iterator.h>
 #include <vector>
@@ -49,9 +50,9 @@ __global__ void k_cand_flags(VarPred p, uint32_t nv, uint8_t *flag) {
 }
 
 __global__ void k_pair_flags(const uint32_t *src, const uint32_t *dst, uint64_t n, VarPred py, int same,
-                             uint8_t *flag) {
+                             uint8_t *flag, VarPred px, int check_src) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        flag[i] = py.ok(dst[i]) && (!same || src[i] == dst[i]);
+        flag[i] = py.ok(dst[i]) && (!same || src[i] == dst[i]) && (!check_src || px.ok(src[i]));
 }
 
 __device__ __forceinline__ uint64_t lower_bound_u32(const uint32_t *a, uint64_t n, uint32_t key) {
@@ -270,16 +271,30 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
         const rpq_nfa *nfa = q->atom_nfa[ai];
         const int cx = T.col_of(x), cy = T.col_of(y);
         // ---- sources of the atom ----
+        // Backward (reverse plan): x free and unconstrained by a
+        // constant, y bound or constant, in-edges loaded -> evaluate the
+        // reversed automaton over the transposed graph from y's values; the
+        // relation then comes sorted by (y, x).
+        const bool backward = cx < 0 && vcst[x] < 0 && (cy >= 0 || vcst[y] >= 0) &&
+                              g->in_csr.size() == g->csr.size() && !getenv("RPQ_CRPQ_FORWARD");
+        const uint32_t sv = backward ? y : x;      // the side the traversal starts from
+        const int csv = backward ? cy : cx;
+        rpq_nfa *rev_nfa = nullptr;
+        struct RevGuard { rpq_nfa **p; ~RevGuard() { delete *p; } } revg{&rev_nfa};
+        if (backward) {
+            rpq_status rs = reverse_automaton(nfa, &rev_nfa);
+            if (rs != RPQ_OK) return rs;
+        }
         uint32_t *srcs = nullptr;
         uint64_t nsrc = 0;
         bool all_v = false;
-        if (cx >= 0) {
+        if (csv >= 0) {
             // distinct values bound to x
             uint32_t *tmpk = (uint32_t *)P.get(T.n * 4), *sorted = (uint32_t *)P.get(T.n * 4);
             srcs = (uint32_t *)P.get(T.n * 4);
             uint64_t *d_n = (uint64_t *)P.get(8);
             if (!tmpk || !sorted || !srcs || !d_n) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
-            RPQ_CUDA_TRY(cudaMemcpyAsync(tmpk, T.cols[cx], T.n * 4, cudaMemcpyDeviceToDevice, s));
+            RPQ_CUDA_TRY(cudaMemcpyAsync(tmpk, T.cols[csv], T.n * 4, cudaMemcpyDeviceToDevice, s));
             size_t t1 = 0, t2 = 0;
             cub::DeviceRadixSort::SortKeys(nullptr, t1, tmpk, sorted, (int64_t)T.n, 0, 32, s);
             cub::DeviceSelect::Unique(nullptr, t2, sorted, srcs, d_n, (int64_t)T.n, s);
@@ -289,19 +304,19 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
             cub::DeviceSelect::Unique(tmp, t2, sorted, srcs, d_n, (int64_t)T.n, s);
             RPQ_CUDA_TRY(cudaMemcpyAsync(&nsrc, d_n, 8, cudaMemcpyDeviceToHost, s));
             RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        } else if (vcst[x] >= 0) {
+        } else if (vcst[sv] >= 0) {
             srcs = (uint32_t *)P.get(4);
             if (!srcs) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
-            const uint32_t c = (uint32_t)vcst[x];
+            const uint32_t c = (uint32_t)vcst[sv];
             RPQ_CUDA_TRY(cudaMemcpyAsync(srcs, &c, 4, cudaMemcpyHostToDevice, s));
             RPQ_CUDA_TRY(cudaStreamSynchronize(s));
             nsrc = 1;
-        } else if (vlab[x] >= 0) {
+        } else if (vlab[sv] >= 0) {
             uint8_t *flag = (uint8_t *)P.get(g->nv);
             srcs = (uint32_t *)P.get((uint64_t)g->nv * 4);
             uint64_t *d_n = (uint64_t *)P.get(8);
             if (!flag || !srcs || !d_n) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
-            k_cand_flags<<<grid_for(g->nv), 256, 0, s>>>(pred(x), g->nv, flag);
+            k_cand_flags<<<grid_for(g->nv), 256, 0, s>>>(pred(sv), g->nv, flag);
             size_t tb = 0;
             thrust::counting_iterator<uint32_t> it(0);
             cub::DeviceSelect::Flagged(nullptr, tb, it, flag, srcs, d_n, (int64_t)g->nv, s);
@@ -318,14 +333,18 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
         ao.mode = RPQ_PAIRS | (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS));
         ao.shard_index = 0;
         ao.shard_count = 1;
+        if (backward) ao.reserved |= 2u;           // in-edge CSR (transposed graph)
+        const rpq_nfa *enfa = backward ? rev_nfa : nfa;
         rpq_result *rel = nullptr;
-        rpq_status st = all_v ? eval_sources_device(g, nfa, nullptr, 0, &ao, &rel)
-                              : eval_sources_device(g, nfa, srcs, nsrc, &ao, &rel);
+        rpq_status st = all_v ? eval_sources_device(g, enfa, nullptr, 0, &ao, &rel)
+                              : eval_sources_device(g, enfa, srcs, nsrc, &ao, &rel);
         if (st != RPQ_OK) return st;
         add_stats(ST, rel->stats);
         struct RelGuard { rpq_result *r; ~RelGuard() { rpq_result_release(r); } } rg{rel};
         uint64_t nrel = rel->nrows;
-        std::vector<uint32_t *> rc = {rel->cols[0], rel->cols[1]};
+        // (x, y) columns; backward results are (y, x) pairs sorted by (y, x)
+        std::vector<uint32_t *> rc = backward ? std::vector<uint32_t *>{rel->cols[1], rel->cols[0]}
+                                              : std::vector<uint32_t *>{rel->cols[0], rel->cols[1]};
         // own the columns in the pool (so compaction can replace them)
         for (auto &c : rc) {
             uint32_t *o2 = (uint32_t *)P.get(std::max<uint64_t>(nrel, 1) * 4);
@@ -337,7 +356,8 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
         if (nrel) {
             uint8_t *flag = (uint8_t *)P.get(nrel);
             if (!flag) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
-            k_pair_flags<<<grid_for(nrel), 256, 0, s>>>(rc[0], rc[1], nrel, pred(y), x == y ? 1 : 0, flag);
+            k_pair_flags<<<grid_for(nrel), 256, 0, s>>>(rc[0], rc[1], nrel, pred(y), x == y ? 1 : 0, flag, pred(x),
+                                                        backward ? 1 : 0);
             st = compact(P, rc, nrel, flag, s);
             if (st != RPQ_OK) return st;
         }
@@ -362,7 +382,7 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
         // one endpoint bound: key column of the relation must be sorted
         const bool by_src = cx >= 0;
         uint32_t *rkey = rc[0], *rval = rc[1];
-        if (!by_src && nrel) {
+        if (!by_src && nrel && !backward) {       // (backward relations are already sorted by y)
             uint64_t *k1 = (uint64_t *)P.get(nrel * 8), *k2 = (uint64_t *)P.get(nrel * 8);
             if (!k1 || !k2) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
             k_pack_swap<<<grid_for(nrel), 256, 0, s>>>(rc[0], rc[1], nrel, k1);
@@ -372,6 +392,9 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
             if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
             cub::DeviceRadixSort::SortKeys(tmp, tb, k1, k2, (int64_t)nrel, 0, 64, s);
             k_unpack<<<grid_for(nrel), 256, 0, s>>>(k2, nrel, rc[1], rc[0]);   // rc[1] = dst (key), rc[0] = src
+            rkey = rc[1];
+            rval = rc[0];
+        } else if (!by_src) {
             rkey = rc[1];
             rval = rc[0];
         }

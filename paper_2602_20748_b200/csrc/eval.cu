@@ -646,6 +646,30 @@ __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layo
             const int slot = A.tslot[t];
             const uint32_t beg = __ldg(A.off[slot] + sv), end = __ldg(A.off[slot] + sv + 1);
             if (STATS && lane == 0) st[S_ITEM_TRANS]++;
+            if (end - beg > HUB_EDGES) {
+                // long seed row (e.g. a single target with 10^5 in-edges):
+                // its HUB_EDGES segments go to k_level_hub, launched next
+                uint32_t hs = 0;
+                if (lane == 0) hs = atomicAdd(&p.ctrl->nhub_items, 1u);
+                hs = __shfl_sync(0xffffffffu, hs, 0);
+                const uint32_t nseg = (end - beg + HUB_EDGES - 1) / HUB_EDGES;
+                uint32_t r = 0;
+                if (hs < p.hitem_cap && lane == 0) r = atomicAdd(&p.ctrl->nhub_recs, nseg);
+                r = __shfl_sync(0xffffffffu, r, 0);
+                if (hs < p.hitem_cap && r + nseg <= p.hrec_cap) {
+#pragma unroll
+                    for (int k = 0; k < KGRP; ++k) p.hubF[((uint64_t)hs * KGRP + k) * 32 + lane] = f[k];
+                    if (lane == 0) p.hitems[hs] = HubItem{0u, xw, 1u, bits};
+                    for (uint32_t sg = lane; sg < nseg; sg += 32) {
+                        const uint32_t s0 = beg + sg * HUB_EDGES;
+                        p.hrecs[r + sg] = HubRec{hs, (uint32_t)t, s0, min(end, s0 + HUB_EDGES)};
+                    }
+                    continue;
+                }
+                if (hs < p.hitem_cap)   // records did not fit: neutralise the reserved ones
+                    for (uint32_t sg = lane; r + sg < p.hrec_cap && sg < nseg; sg += 32)
+                        p.hrecs[r + sg] = HubRec{0u, 0u, 0u, 0u};
+            }
             if (end > beg)
                 expand_edges<1, STATS>(p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act,
                                        A.toff[A.tto[t] + 1] > A.toff[A.tto[t]]);
@@ -1970,9 +1994,14 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         ST.kernel_launches++;
         if (skip_q0) {
             const int sg = grid_for((uint64_t)nb * 32, 256, 148 * 8);
-            if (stats) k_seed_expand<true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
-            else k_seed_expand<false><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
-            ST.kernel_launches++;
+            if (stats) {
+                k_seed_expand<true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
+                k_level_hub<true><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
+            } else {
+                k_seed_expand<false><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
+                k_level_hub<false><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
+            }
+            ST.kernel_launches += 2;
         }
         PT.mark("seed");
         rpq_status st = RPQ_OK;

@@ -20,9 +20,10 @@ def rows(res):
     return [tuple(r) for r in res.rows().tolist()]
 
 
-def test_q2_paper_tuples(toy):
+@pytest.mark.parametrize("ie", [False, True])
+def test_q2_paper_tuples(toy, ie):
     """Q2 -> 4 tuples; with distinct(u2,u4) -> 2."""
-    G = R.rpq_graph_load(toy)
+    G = R.rpq_graph_load(toy, in_edges=ie)
     atoms = [("u3", "ab", "u2"), ("u3", "ab", "u4"), ("u2", "c*", "u4")]
     lab = {"u2": "D", "u3": "A", "u4": "D"}
     r = R.crpq(G, ["u2", "u3", "u4"], atoms, var_label=lab)
@@ -31,8 +32,9 @@ def test_q2_paper_tuples(toy):
     assert rows(r) == [(10, 0, 12), (12, 0, 10)]
 
 
-def test_constant_and_self_atom(toy):
-    G = R.rpq_graph_load(toy)
+@pytest.mark.parametrize("ie", [False, True])
+def test_constant_and_self_atom(toy, ie):
+    G = R.rpq_graph_load(toy, in_edges=ie)
     # x -c+-> x on the toy graph: vertices on c-cycles
     r = R.crpq(G, ["x"], [("x", "c+", "x")])
     want = oracle.crpq_bruteforce(toy, oracle.CRPQ(["x"], [("x", "c+", "x")]))
@@ -43,13 +45,14 @@ def test_constant_and_self_atom(toy):
     assert rows(r) == oracle.crpq_bruteforce(toy, q)
 
 
+@pytest.mark.parametrize("ie", [False, True])
 @pytest.mark.parametrize("seed", range(8))
-def test_random_crpqs_vs_bruteforce(seed):
+def test_random_crpqs_vs_bruteforce(seed, ie):
     rng = np.random.default_rng(seed)
     g = synth.random_small(rng, max_v=7, max_e=16, num_labels=3, min_v=3)
     g.vertex_label = rng.integers(0, 2, g.num_vertices).astype(np.uint16)
     g.vertex_label_names = ["P", "Q"]
-    G = R.rpq_graph_load(g)
+    G = R.rpq_graph_load(g, in_edges=ie)
     shapes = [
         (["x", "y", "z"], [("x", "a b*", "y"), ("y", "c*", "z"), ("x", "(a|c)+", "z")], {"x": "P"}, [("x", "z")]),
         (["x", "y", "z"], [("x", "a", "y"), ("x", "b*", "z")], {}, []),                          # star
@@ -75,13 +78,14 @@ def test_crpq_errors(toy):
     assert e.value.status == R.RPQ_EUNSUPPORTED
 
 
-def test_cfg4_ldbc_crpq_small():
+@pytest.mark.parametrize("ie", [False, True])
+def test_cfg4_ldbc_crpq_small(ie):
     """BASELINE cfg4 shape: m -hasTag-> t:Sports, m -hasCreator-> u,
     m -replyOf*-> p:Post.  Against the oracle's hash join of O1 relations and
     the closed form (one tuple per Sports-tagged message: one creator, one
     root post)."""
     g = synth.ldbc_graph(0.002)
-    G = R.rpq_graph_load(g)
+    G = R.rpq_graph_load(g, in_edges=ie)
     sports = g.meta["sports"]
     vars_ = ["m", "t", "u", "p"]
     atoms = [("m", "hasTag", "t"), ("m", "hasCreator", "u"), ("m", "replyOf*", "p")]

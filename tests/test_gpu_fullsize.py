@@ -55,7 +55,7 @@ def reply_depths(g):
 @pytest.fixture(scope="module")
 def ldbc():
     g = synth.ldbc_graph(1.0, seed=10)          # bench.py --workload cfg3
-    G = R.rpq_graph_load(g)
+    G = R.rpq_graph_load(g, in_edges=True)      # cfg4's Sports atom runs backward
     return g, G
 
 
