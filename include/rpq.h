@@ -230,6 +230,9 @@ typedef struct {
     uint64_t kernel_launches;   /* all kernels this library launched for the call */
     double expand_ms;           /* RPQ_TIME_KERNELS: summed CUDA-event time of expand launches */
     double total_ms;            /* CUDA-event time from entry to result ready */
+    uint64_t pull_levels;       /* levels run bottom-up (direction-optimising), over batches */
+    uint64_t pull_loads;        /* in-neighbour visited-word loads of the pull levels */
+    uint64_t pull_words;        /* (row, word) pairs scanned by the pull levels */
 } rpq_stats;
 
 uint64_t rpq_result_count(const rpq_result *r);

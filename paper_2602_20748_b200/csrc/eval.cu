@@ -55,7 +55,7 @@ constexpr int MAXT = RPQ_MAX_TRANSITIONS;
 constexpr int MAXL = RPQ_MAX_QUERY_LABELS;
 constexpr uint32_t HUB_EDGES = 512;      // edges per hub segment
 constexpr int TILE_V = 1024;             // vertices per extraction tile
-constexpr int NSTAT = 8;
+constexpr int NSTAT = 12;
 #ifndef RPQ_LEVEL_MINB
 #define RPQ_LEVEL_MINB 5
 #endif
@@ -79,6 +79,13 @@ struct DevAuto {
     uint8_t tto[MAXT];
     const uint32_t *off[MAXL];
     const uint32_t *nbr[MAXL];
+    // pull (bottom-up) levels: transitions grouped by TARGET state and the
+    // transposed CSR of every label slot (null when not loaded)
+    uint16_t itoff[MAXQ + 1];
+    uint8_t itfrom[MAXT];
+    uint8_t itslot[MAXT];
+    const uint32_t *ioff[MAXL];
+    const uint32_t *inbr[MAXL];
 };
 
 struct Layout {
@@ -108,7 +115,13 @@ struct Ctrl {                  // per-level device counters / flags
     uint32_t ucnt[2];          // active work units listed for the level of each parity
     uint32_t ucur[2];          // work-unit cursor (dynamic fetch) per parity
     uint32_t ntouched;         // entries of LevelArgs::TL
-    uint32_t pad[2];
+    uint32_t pcur[2];          // pull-level task cursor per parity
+    // adaptive direction: a pull level counts the chunk-words that needed bits
+    // and those it completed; if fewer than half complete (directed graphs
+    // where most sources never reach most vertices), the batch stays top-down
+    unsigned long long pull_need, pull_done;
+    uint32_t pull_off;
+    uint32_t pad;
 };
 
 // One BFS level over the rows whose activity bit is set in (Xcur, XBcur).
@@ -135,10 +148,18 @@ struct LevelArgs {
     uint32_t *TU;              // touched work units of the batch (bitmap) ...
     uint32_t *TL;              // ... and their list (ctrl->ntouched entries)
     unsigned long long *stats;
+    // direction-optimising levels: per column word, the sources
+    // that may still gain bits (a superset: OR of the frontier words of the
+    // level, or the exact new bits of a pull level); cur = this level's
+    // filter, next = accumulated for the following level
+    uint64_t *ActCur, *ActNext;
+    uint64_t total_units;      // work units of the whole state (direction heuristic)
+    uint32_t pull_mode;        // 0: top-down only; 1: bottom-up on dense levels
 };
 
 // stats slots
-enum { S_PE = 0, S_WORD_ITEMS, S_WORD_EDGE, S_ITEMS, S_ITEM_EDGES, S_ITEM_TRANS, S_X_RED, S_N_RED };
+enum { S_PE = 0, S_WORD_ITEMS, S_WORD_EDGE, S_ITEMS, S_ITEM_EDGES, S_ITEM_TRANS, S_X_RED, S_N_RED, S_PULL_LEVELS,
+       S_PULL_LOADS, S_PULL_WORDS, S_PE_POST };
 
 __device__ __forceinline__ uint64_t ld_cg(const uint64_t *p) { return __ldcg((const unsigned long long *)p); }
 
@@ -148,6 +169,33 @@ __device__ __forceinline__ void red_or64(uint64_t *p, uint64_t v) {
 }
 __device__ __forceinline__ void red_or32(uint32_t *p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.or.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Direction of the level of parity p.par, decided identically by every kernel
+// of the level from the active-unit count that k_units produced.
+// Bottom-up when enabled for the query (symmetric relations, or forced) and
+// at least 10 % of the work units are active (a dense frontier).
+__device__ __forceinline__ bool level_pull(const LevelArgs &p) {
+    if (!p.pull_mode || *(volatile const uint32_t *)&p.ctrl->pull_off) return false;
+    const uint32_t n = *(volatile const uint32_t *)&p.ctrl->ucnt[p.par];
+    return n != 0 && (uint64_t)n * 10ull > p.total_units;
+}
+
+// per-CTA accumulation of the activity columns in shared memory, flushed with
+// one global OR per word and CTA (the column words are few and hot)
+constexpr uint32_t ACT_SMEM_WORDS = 2048;
+__device__ __forceinline__ void act_init(unsigned long long *actS, uint32_t nw) {
+    for (uint32_t i = threadIdx.x; i < nw && i < ACT_SMEM_WORDS; i += blockDim.x) actS[i] = 0ull;
+    __syncthreads();
+}
+__device__ __forceinline__ void act_or(unsigned long long *actS, uint64_t *g, uint32_t col, uint64_t m) {
+    if (col < ACT_SMEM_WORDS) atomicOr(actS + col, (unsigned long long)m);
+    else red_or64(g + col, m);
+}
+__device__ __forceinline__ void act_flush(const unsigned long long *actS, uint64_t *g, uint32_t nw) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nw && i < ACT_SMEM_WORDS; i += blockDim.x)
+        if (actS[i]) red_or64(g + i, actS[i]);
 }
 
 // the per-batch layout lives in device memory (so a captured level graph is
@@ -175,11 +223,17 @@ __global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         p.ctrl->ucnt[par ^ 1] = 0;
         p.ctrl->ucur[par ^ 1] = 0;
+        p.ctrl->pcur[par] = 0;
         p.ctrl->active[par ^ 1] = 0;   // set by this level's activations
+        p.ctrl->pull_need = p.ctrl->pull_done = 0;
+
         p.ctrl->nhub_items = 0;
         p.ctrl->nhub_recs = 0;
         p.ctrl->levels += 1;
     }
+    if (p.pull_mode)   // the previous level's filter, free now: this level accumulates into it
+        for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.nw; i += (uint64_t)gridDim.x * blockDim.x)
+            p.ActNext[i] = 0ull;
     const int lane = threadIdx.x & 31;
     for (uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; w0 < nxbwords;
          w0 += (uint64_t)gridDim.x * blockDim.x) {
@@ -431,13 +485,16 @@ __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const
 template <bool STATS>
 __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, const Layout *__restrict__ Sg,
                                                                const LevelArgs p) {
+    if (level_pull(p)) return;                 // bottom-up level: k_pull_prep + k_pull
     __shared__ Layout S;
+    __shared__ unsigned long long actS[ACT_SMEM_WORDS];
     load_layout(S, Sg, A.nq);
+    if (p.pull_mode) act_init(actS, p.nw);
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
     const uint32_t nunits = *(volatile uint32_t *)&p.ctrl->ucnt[p.par];
-    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long st[NSTAT] = {};
     bool act = false;
     (void)wid;
     // Few active units (small row counts, e.g. knows+ over 65 K persons, or
@@ -506,6 +563,8 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                     f[k] &= ~dd[k];
                     if (f[k]) {
                         p.Done[rb + bt * p.cw] = dd[k] | f[k];
+                        // sources of this frontier word may gain bits next level
+                        if (p.pull_mode) act_or(actS, p.ActNext, (uint32_t)(rb - row * p.nw) + bt * p.cw, f[k]);
                         if (STATS) st[S_WORD_ITEMS]++;
                     }
                 }
@@ -563,6 +622,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
     }
     if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
     flush_stats<STATS>(st, p.stats);
+    if (p.pull_mode) act_flush(actS, p.ActNext, p.nw);
 }
 
 // Deferred long rows: a warp per HUB_EDGES-edge segment.
@@ -575,7 +635,7 @@ __global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
     const uint32_t n = min(p.ctrl->nhub_recs, p.hrec_cap);
-    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long st[NSTAT] = {};
     bool act = false;
     for (uint64_t it = wid; it < n; it += nwarps) {
         const HubRec r = p.hrecs[it];
@@ -591,6 +651,199 @@ __global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A
     flush_stats<STATS>(st, p.stats);
 }
 
+// ---- bottom-up (pull) levels: direction-optimising BFS --------
+// A level whose active-unit fraction exceeds the threshold runs bottom-up:
+// every (target row, 32-word chunk) with sources that are still active and
+// have not reached it (need = Act & ~Vis) ORs the visited words of its
+// in-neighbours (transposed CSR, entering transitions) until need is
+// covered, then writes the new bits with a plain store -- one owner per
+// word, no atomics, early exit once the row is complete (the dense levels of
+// knows+, where most rows fill from their first in-neighbours).  Reading Vis
+// (not the frontier) of the in-neighbours is exact: bits of Vis that are not
+// in the frontier were already propagated along every out-edge.
+
+// Before a pull level: consume the level's activity (X words -> TX) and mark
+// every bit of the active chunks expanded (Done = Vis): the pull propagates
+// all of Vis, so afterwards the frontier is exactly the new bits.
+__global__ void k_pull_prep(const DevAuto A, const LevelArgs p) {
+    if (!level_pull(p)) return;
+    const int lane = threadIdx.x & 31;
+    const uint32_t nunits = *(volatile uint32_t *)&p.ctrl->ucnt[p.par];
+    for (;;) {
+        uint32_t ui = 0;
+        if (lane == 0) ui = atomicAdd(&p.ctrl->ucur[p.par], 1u);
+        ui = __shfl_sync(0xffffffffu, ui, 0);
+        if (ui >= nunits) break;
+        const uint64_t u = p.ulist[ui];
+        const uint64_t xi_l = u * 32 + lane;
+        const uint32_t xl = xi_l < p.nxwords ? __ldcg(p.Xcur + xi_l) : 0u;
+        if (xl) {
+            p.Xcur[xi_l] = 0u;
+            p.TX[xi_l] |= xl;
+        }
+        unsigned todo = __ballot_sync(0xffffffffu, xl != 0);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            uint32_t x = __shfl_sync(0xffffffffu, xl, src);
+            const uint64_t xi = u * 32 + src;
+            const uint64_t row = xi / p.nxw;
+            const uint32_t xw = (uint32_t)(xi % p.nxw);
+            while (x) {
+                const uint32_t bt = (uint32_t)(__ffs(x) - 1);
+                x &= x - 1;
+                const uint64_t col = (uint64_t)(xw * 32u + bt) * 32u + lane;   // cw == 32
+                if (col < p.nw) p.Done[row * p.nw + col] = ld_cg(p.Vis + row * p.nw + col);
+            }
+        }
+    }
+}
+
+// OR of the in-neighbours' visited words of column col for target (q2, v),
+// stopping as soon as every needed bit is covered (8 loads in flight).
+template <bool STATS>
+__device__ __forceinline__ uint64_t pull_gather(const DevAuto &A, const Layout &S, const LevelArgs &p, int q2,
+                                                uint32_t v, uint32_t col, uint64_t need, int lane,
+                                                unsigned long long *st, uint32_t *visited = nullptr) {
+    const int it0 = A.itoff[q2], it1 = A.itoff[q2 + 1];
+    uint64_t acc = 0;
+    uint32_t nvis = 0;
+    for (int it = it0; it < it1 && __any_sync(0xffffffffu, (need & ~acc) != 0); ++it) {
+        const int q = A.itfrom[it], slot = A.itslot[it];
+        const uint32_t beg = __ldg(A.ioff[slot] + v), end = __ldg(A.ioff[slot] + v + 1);
+        const uint32_t lo = S.lo[q], len = S.len[q];
+        const uint64_t tb = S.row_base[q] - lo;
+        for (uint32_t j = beg; j < end; j += 32) {
+            const uint32_t my = (j + lane < end) ? __ldg(A.inbr[slot] + j + lane) : 0u;
+            const int cnt = (int)min(32u, end - j);
+            bool done = false;
+            for (int e0 = 0; e0 < cnt && !done; e0 += 8) {
+                const bool want = (need & ~acc) != 0;
+                uint64_t x[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const uint32_t u = __shfl_sync(0xffffffffu, my, (e0 + e) & 31);
+                    const bool ok = want && e0 + e < cnt && u - lo < len;
+                    x[e] = ok ? ld_cg(p.Vis + (tb + u) * p.nw + col) : 0ull;
+                    if (STATS && ok) st[S_PULL_LOADS]++;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc |= x[e];
+                nvis += (uint32_t)min(8, cnt - e0);
+                done = !__any_sync(0xffffffffu, (need & ~acc) != 0);
+            }
+            if (done) break;
+        }
+    }
+    if (visited) *visited = nvis;
+    return acc;
+}
+
+constexpr uint32_t PULL_TASKS = 32;   // (chunk, row) tasks per cursor fetch
+
+template <bool STATS>
+__global__ void __launch_bounds__(256) k_pull(const DevAuto A, const Layout *__restrict__ Sg, const LevelArgs p) {
+    if (!level_pull(p)) return;
+    __shared__ Layout S;
+    __shared__ unsigned long long actS[ACT_SMEM_WORDS];
+    load_layout(S, Sg, A.nq);
+    act_init(actS, p.nw);
+    const int lane = threadIdx.x & 31;
+    const uint64_t nrows = S.row_base[A.nq - 1] + S.len[A.nq - 1];
+    const uint32_t nch = p.nw / 32u;
+    const uint64_t ntask = nrows * nch;
+    unsigned long long st[NSTAT] = {};
+    unsigned long long cnt_need = 0, cnt_done = 0;
+    bool act = false;
+    for (;;) {
+        uint32_t t0 = 0;
+        if (lane == 0) t0 = atomicAdd(&p.ctrl->pcur[p.par], PULL_TASKS);
+        t0 = __shfl_sync(0xffffffffu, t0, 0);
+        if (t0 >= ntask) break;
+        const uint64_t t1 = ntask < (uint64_t)t0 + PULL_TASKS ? ntask : (uint64_t)t0 + PULL_TASKS;
+        for (uint64_t t = t0; t < t1; ++t) {
+            const uint32_t c = (uint32_t)(t / nrows);          // chunk-major: a run of rows per chunk
+            const uint64_t row = t - (uint64_t)c * nrows;
+            const int q2 = row_state(S, A.nq, row);
+            const int it0 = A.itoff[q2], it1 = A.itoff[q2 + 1];
+            if (it0 == it1) continue;                            // nothing enters q2
+            const uint32_t col = c * 32u + lane;
+            const uint64_t wi = row * p.nw + col;
+            if (STATS && lane == 0) st[S_PULL_WORDS] += 32;
+            const uint64_t vis = ld_cg(p.Vis + wi);
+            const uint64_t need = ld_cg(p.ActCur + col) & ~vis;
+            if (!__any_sync(0xffffffffu, need != 0)) continue;
+            const uint32_t v = S.lo[q2] + (uint32_t)(row - S.row_base[q2]);
+            const uint64_t acc = pull_gather<STATS>(A, S, p, q2, v, col, need, lane, st);
+            const uint64_t nb = need & acc;
+            {   // words that needed bits / that this level completed
+                const unsigned nm = __ballot_sync(0xffffffffu, need != 0);
+                const unsigned fm = __ballot_sync(0xffffffffu, need != 0 && nb == need);
+                if (lane == 0) { cnt_need += __popc(nm); cnt_done += __popc(fm); }
+            }
+            if (nb) {
+                p.Vis[wi] = vis | nb;                      // single owner of the word in a pull level
+                act_or(actS, p.ActNext, col, nb);
+            }
+            if (__any_sync(0xffffffffu, nb != 0) && lane == 0 && A.toff[q2 + 1] > A.toff[q2]) {
+                const uint64_t xi = row * p.nxw + c / 32u;
+                red_or32(p.Xnext + xi, 1u << (c & 31u));
+                red_or32(p.XBnext + (xi >> 10), 1u << ((xi >> 5) & 31));
+                act = true;
+            }
+        }
+    }
+    if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
+    if (lane == 0 && cnt_need) {
+        atomicAdd(&p.ctrl->pull_need, cnt_need);
+        atomicAdd(&p.ctrl->pull_done, cnt_done);
+    }
+    if (STATS && threadIdx.x == 0 && blockIdx.x == 0) st[S_PULL_LEVELS] = 1;
+    flush_stats<STATS>(st, p.stats);
+    act_flush(actS, p.ActNext, p.nw);
+}
+
+// PE after the fact (RPQ_STATS; reading R12): sum over rows (q, v) of
+// popcount(Vis) x product out-degree of (v, q).  Exact whatever the
+// direction of each level (pull levels do not expand bits one by one).
+__global__ void k_pe_rows(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t nw,
+                          unsigned long long *out) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    const uint64_t nrows = S.row_base[A.nq - 1] + S.len[A.nq - 1];
+    unsigned long long acc = 0;
+    for (uint64_t row = wid; row < nrows; row += nwarps) {
+        const int q = row_state(S, A.nq, row);
+        if (A.toff[q + 1] == A.toff[q]) continue;
+        const uint32_t v = S.lo[q] + (uint32_t)(row - S.row_base[q]);
+        unsigned long long pc = 0;
+        for (uint32_t w = lane; w < nw; w += 32) pc += __popcll(ld_cg(Vis + row * nw + w));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) pc += __shfl_xor_sync(0xffffffffu, pc, o);
+        if (!pc) continue;
+        unsigned long long deg = 0;
+        for (int t = A.toff[q]; t < A.toff[q + 1]; ++t)
+            deg += __ldg(A.off[A.tslot[t]] + v + 1) - __ldg(A.off[A.tslot[t]] + v);
+        acc += pc * deg;
+    }
+    if (lane == 0 && acc) atomicAdd(out, acc);
+}
+
+// PE of the seeds when q0 has no rows (k_seed_expand): out-degree of (s, q0).
+__global__ void k_pe_seeds(const DevAuto A, const uint32_t *cand, const uint32_t *pidx, uint64_t b0, uint32_t nb,
+                           unsigned long long *out) {
+    unsigned long long acc = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+        const uint32_t sv = cand[pidx[b0 + i]];
+        for (int t = A.toff[0]; t < A.toff[1]; ++t)
+            acc += __ldg(A.off[A.tslot[t]] + sv + 1) - __ldg(A.off[A.tslot[t]] + sv);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 // Seed batch sources: source i of the batch gets bit i in N of row (q0, s_i)
 // and its chunk is marked active; the first level moves it into Vis.  With
 // `skip_q0` (q0 has no incoming transition and is not final, so its rows
@@ -598,7 +851,11 @@ __global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A
 // expands the seeds directly and q0 gets no rows at all.
 __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const uint32_t *__restrict__ pidx,
                        uint64_t b0, uint32_t nb, uint64_t *Vis, uint32_t *X, uint32_t *XB, uint32_t nw, uint32_t nxw,
-                       uint32_t cw, Ctrl *ctrl, int skip_q0) {
+                       uint32_t cw, Ctrl *ctrl, int skip_q0, uint64_t *act0) {
+    // every batch source is active at the first level (pull filter)
+    if (act0)
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x)
+            atomicOr((unsigned long long *)act0 + (i >> 6), 1ull << (i & 63));
     if (!skip_q0)
         for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
             const uint32_t s = cand[pidx[b0 + i]];
@@ -617,6 +874,8 @@ __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const 
         ctrl->ucnt[0] = ctrl->ucnt[1] = 0;
         ctrl->ucur[0] = ctrl->ucur[1] = 0;
         ctrl->ntouched = 0;
+        ctrl->pull_off = 0;
+        ctrl->pull_need = ctrl->pull_done = 0;
     }
 }
 
@@ -632,7 +891,7 @@ __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layo
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    unsigned long long st[NSTAT] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long st[NSTAT] = {};
     bool act = false;
     for (uint64_t i = wid; i < nb; i += nwarps) {
         const uint32_t sv = cand[pidx[b0 + i]];
@@ -1269,6 +1528,51 @@ inline int grid_for(uint64_t threads, int block = 256, int cap = 148 * 16) {
     return g ? (int)g : 1;
 }
 
+// Symmetry of one label's edge set: a warp per row u, every neighbour w
+// binary-searches u in w's (sorted) row.
+__global__ void k_sym_check(const uint32_t *off, const uint32_t *nbr, uint32_t nv, int *bad) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    for (uint64_t u = wid; u < nv; u += nwarps) {
+        if (*(volatile int *)bad) return;
+        const uint32_t b = off[u], e = off[u + 1];
+        bool ok = true;
+        for (uint32_t j = b + lane; j < e; j += 32) {
+            const uint32_t w = nbr[j];
+            uint32_t lo = off[w], hi = off[w + 1];
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (nbr[mid] < (uint32_t)u) lo = mid + 1; else hi = mid;
+            }
+            ok &= lo < off[w + 1] && nbr[lo] == (uint32_t)u;
+        }
+        if (!__all_sync(0xffffffffu, ok)) {
+            if (lane == 0) atomicExch(bad, 1);
+            return;
+        }
+    }
+}
+
+// Cached per graph and label (first use only; not query work after that).
+bool label_symmetric(const rpq_graph *g, uint32_t l, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g->sym_mu);
+    if (g->sym.size() != g->csr.size()) g->sym.assign(g->csr.size(), -1);
+    if (g->sym[l] >= 0) return g->sym[l] != 0;
+    int *d_bad = (int *)dev_alloc(sizeof(int), s);
+    int bad = 1;
+    if (d_bad && cudaMemsetAsync(d_bad, 0, sizeof(int), s) == cudaSuccess) {
+        k_sym_check<<<148 * 8, 256, 0, s>>>(g->csr[l].off, g->csr[l].nbr, g->nv, d_bad);
+        if (cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            bad = 1;
+    }
+    cudaGetLastError();
+    dev_free(d_bad, s);
+    g->sym[l] = bad ? 0 : 1;
+    return !bad;
+}
+
 // ---- host-side evaluation driver ------------------------------------------
 struct Workspace {
     cudaStream_t s;
@@ -1338,15 +1642,22 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
     uint64_t nxb = nxbwords;
     void *a0[] = {&a, &sg, &p0};
     void *a1[] = {&a, &sg, &p1};
+    void *r0[] = {&a, &p0};
+    void *r1[] = {&a, &p1};
     void *u0[] = {&p0, &nxb};
     void *u1[] = {&p1, &nxb};
     void *m1[] = {&ctrl, &h};
     const int ugrid = (int)std::min<uint64_t>(148 * 4, (nxbwords + 255) / 256 + 1);
+    const bool pull = P0.pull_mode != 0;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u0)) != cudaSuccess) return e;
+    if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r0)) != cudaSuccess) return e;
     if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a0)) != cudaSuccess) return e;
+    if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a0)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u1)) != cudaSuccess) return e;
+    if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a1)) != cudaSuccess) return e;
+    if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_end, dim3(1), dim3(1), m1)) != cudaSuccess) return e;
     return cudaGraphInstantiate(&LG.exec, LG.g, 0);
@@ -1362,11 +1673,14 @@ rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &
     for (;;) {
         const LevelArgs &P = par ? P1 : P0;
         k_units<<<ugrid, 256, 0, s>>>(P, nxbwords);
+        if (P.pull_mode) k_pull_prep<<<148 * 8, 256, 0, s>>>(A, P);
         if (stats) {
             k_level<true><<<grid, 256, 0, s>>>(A, Sg, P);
+            if (P.pull_mode) k_pull<true><<<148 * 8, 256, 0, s>>>(A, Sg, P);
             k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
         } else {
             k_level<false><<<grid, 256, 0, s>>>(A, Sg, P);
+            if (P.pull_mode) k_pull<false><<<148 * 8, 256, 0, s>>>(A, Sg, P);
             k_level_hub<false><<<hgrid, 256, 0, s>>>(A, Sg, P);
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(h_flag, &P.ctrl->active[par ^ 1], 4, cudaMemcpyDeviceToHost, s));
@@ -1442,9 +1756,39 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     if (reverse && g->in_csr.size() != g->csr.size())
         return fail(rpq_fail(RPQ_EUNSUPPORTED, "graph loaded without RPQ_GRAPH_IN_EDGES"));
     const std::vector<LabelCSR> &CSR = reverse ? g->in_csr : g->csr;
+    // Bottom-up (pull) levels need each label's transposed CSR.  Default:
+    // only when every label of the query is symmetric (undirected relations
+    // such as knows: BFS rows then fill from their first in-neighbours, and
+    // the transposed CSR is the CSR itself); RPQ_PULL=always also uses the
+    // in-edge CSR of directed labels; RPQ_PULL=never disables it.  (On the
+    // directed cfg2 / RMAT queries bottom-up levels measured 1.3-2x slower
+    // than top-down ones at every frontier density.)
+    const std::vector<LabelCSR> &TCSR = reverse ? g->csr : g->in_csr;
+    const bool have_t = TCSR.size() == CSR.size();
+    int pull_req = 1;
+    {
+        const char *pm = getenv("RPQ_PULL");
+        if (pm && (!strcmp(pm, "0") || !strcmp(pm, "never"))) pull_req = 0;
+        if (pm && (!strcmp(pm, "2") || !strcmp(pm, "always"))) pull_req = 2;
+    }
+    bool all_sym = pull_req != 0 && !slot_label.empty();
+    for (size_t k = 0; k < slot_label.size() && all_sym; ++k) all_sym = label_symmetric(g, slot_label[k], s);
+    const bool use_t = pull_req == 2 && have_t && !all_sym;
     for (size_t k = 0; k < slot_label.size(); ++k) {
         A.off[k] = CSR[slot_label[k]].off;
         A.nbr[k] = CSR[slot_label[k]].nbr;
+        A.ioff[k] = use_t ? TCSR[slot_label[k]].off : all_sym ? A.off[k] : nullptr;
+        A.inbr[k] = use_t ? TCSR[slot_label[k]].nbr : all_sym ? A.nbr[k] : nullptr;
+    }
+    const bool pull_avail = all_sym || use_t;
+    {   // transitions grouped by target state
+        uint32_t k = 0;
+        for (uint32_t q2 = 0; q2 < a->nq; ++q2) {
+            A.itoff[q2] = (uint16_t)k;
+            for (size_t t = 0; t < a->from.size(); ++t)
+                if (a->to[t] == q2) { A.itfrom[k] = (uint8_t)a->from[t]; A.itslot[k] = A.tslot[t]; ++k; }
+        }
+        A.itoff[a->nq] = (uint16_t)k;
     }
 
     // ---- candidate sources and the productive subset P --------------------
@@ -1890,10 +2234,25 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     P0.stats = d_stats;
     P0.ulist = ulist;
     P0.TX = TX; P0.TU = TU; P0.TL = TL;
+    // direction-optimising levels: need the transposed CSR and 32-word chunks
+    uint64_t *Act = nullptr;
+    {
+        uint32_t mode = pull_avail ? 1u : 0u;
+        if (CW != 32 || !nbatches || sparse_done) mode = 0;
+        if (mode) {
+            Act = (uint64_t *)ws.get(nw * 16);
+            if (!Act) mode = 0;
+        }
+        P0.pull_mode = mode;
+        P0.total_units = nunits;
+        P0.ActCur = Act;
+        P0.ActNext = Act ? Act + nw : nullptr;
+    }
     P1 = P0;
     P1.par = 1;
     std::swap(P1.Xcur, P1.Xnext);
     std::swap(P1.XBcur, P1.XBnext);
+    std::swap(P1.ActCur, P1.ActNext);
     const int lgrid = 148 * RPQ_LEVEL_MINB;   // persistent: warps fetch work units dynamically
     const int hgrid = 148 * RPQ_HUB_MINB;
     LevelGraph LG;
@@ -1989,8 +2348,9 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, d_layouts + lay_i, sizeof(Layout), cudaMemcpyDeviceToDevice, s));
         ++lay_i;
+        if (Act) RPQ_CUDA_TRY(cudaMemsetAsync(Act, 0, nw * 16, s));
         k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, Vis, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl,
-                                            skip_q0 ? 1 : 0);
+                                            skip_q0 ? 1 : 0, Act);
         ST.kernel_launches++;
         if (skip_q0) {
             const int sg = grid_for((uint64_t)nb * 32, 256, 148 * 8);
@@ -2019,6 +2379,11 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         PT.mark("levels");
         HM("levels enqueued");
         if (st != RPQ_OK) return fail(st);
+        if (stats) {   // PE after the fact (exact for push and pull levels alike)
+            k_pe_rows<<<148 * 8, 256, 0, s>>>(A, S, Vis, (uint32_t)nw, d_stats + S_PE_POST);
+            if (skip_q0) k_pe_seeds<<<grid_for(nb), 256, 0, s>>>(A, cand, pidx, b0, nb, d_stats + S_PE_POST);
+            ST.kernel_launches += skip_q0 ? 2 : 1;
+        }
         // X and XB are all zero again here (the last level activated
         // nothing).  Extraction reads Vis of the final states.
         const uint32_t vlo = fin_hull.empty() ? 0 : fin_hull.lo;
@@ -2160,7 +2525,12 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         unsigned long long hs[NSTAT];
         RPQ_CUDA_TRY(cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        ST.product_edges = hs[S_PE] + sub_pe;
+        // dense batches: PE after the fact (k_pe_rows/k_pe_seeds); the sparse
+        // tiers count it per source (S_PE)
+        ST.product_edges = hs[S_PE_POST] + (sparse_done ? hs[S_PE] : 0ull) + sub_pe;
+        ST.pull_levels = hs[S_PULL_LEVELS];
+        ST.pull_loads = hs[S_PULL_LOADS];
+        ST.pull_words = hs[S_PULL_WORDS];
         ST.word_items = hs[S_WORD_ITEMS];
         ST.word_edge_ops = hs[S_WORD_EDGE];
         ST.items = hs[S_ITEMS];

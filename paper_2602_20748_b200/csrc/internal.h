@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -32,6 +33,10 @@ struct rpq_graph {
     std::vector<LabelCSR> in_csr;   // [num_labels] in-edges (RPQ_GRAPH_IN_EDGES), else empty
     uint16_t *vlabel = nullptr;  // device [nv] or null
     std::vector<uint16_t> h_vlabel;   // host copy (CRPQ planning)
+    // per label: is the edge set symmetric ((u,l,w) in E <=> (w,l,u) in E)?
+    // -1 = not checked yet; filled lazily by label_symmetric (eval.cu)
+    mutable std::mutex sym_mu;
+    mutable std::vector<int8_t> sym;
 };
 
 // ---- automaton ("automata plan") ------------------------------

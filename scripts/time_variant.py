@@ -26,7 +26,7 @@ else:
     g = mk()
     np.savez(cache, nv=g.num_vertices, src=g.src, dst=g.dst, label=g.label, names=np.array(g.label_names))
 s = torch.cuda.current_stream()
-G = R.rpq_graph_load(g, stream=s.cuda_stream)
+G = R.rpq_graph_load(g, stream=s.cuda_stream, in_edges=os.environ.get("TV_IN_EDGES") == "1")
 tag = os.path.basename(os.environ.get("RPQ_LIB_PATH", "librpq.so"))
 for rx in qs:
     a = R.rpq_compile(G, rx)
@@ -42,4 +42,7 @@ for rx in qs:
         st = r.stats()
         if best is None or dt < best[0]:
             best = (dt, st["expand_ms"], r.count)
-    print(f"{tag:28s} {rx:10s} total_ms={best[0]:9.2f} loop_ms={best[1]:9.2f} count={best[2]}", flush=True)
+    sp = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=s.cuda_stream, shard_count=shards).stats()
+    print(f"{tag:28s} {rx:10s} total_ms={best[0]:9.2f} loop_ms={best[1]:9.2f} count={best[2]} "
+          f"PE={sp['product_edges']:.4e} pull_levels={sp['pull_levels']} levels={sp['levels']} "
+          f"pull_loads={sp['pull_loads']:.3e} pull_words={sp['pull_words']:.3e}", flush=True)
