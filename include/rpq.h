@@ -181,6 +181,24 @@ rpq_status rpq_eval_targets(const rpq_graph *g, const rpq_nfa *a, const uint32_t
 rpq_status rpq_eval_single_target(const rpq_graph *g, const rpq_nfa *a, uint32_t t,
                                   const rpq_eval_opts *opts, rpq_result **out);
 
+/* Output beyond HBM (the paper's outputs reach 2.4 T pairs
+ * and are materialised through host memory): the
+ * all-pairs result delivered to the host in (src, dst) order through `sink`,
+ * in pieces of at most piece_pairs pairs (0 = 2^26); the host pointers are
+ * valid during the call only.  A PER_SOURCE pass sizes the output; sources
+ * are then evaluated in chunks of consecutive vertex ids whose pairs fit
+ * device_budget_bytes (0 = a quarter of the free device memory; a single
+ * source always forms a chunk), each chunk in PAIRS mode, and its pairs are
+ * copied through two pinned host buffers so that the copy of piece k+1
+ * overlaps the sink of piece k.  Sharding: chunk c belongs to shard
+ * c % shard_count.  *total = pairs delivered.  A sink returning non-zero
+ * stops the evaluation early (RPQ_OK; *total counts what was delivered).
+ * Errors as rpq_eval_allpairs; EINVAL for a NULL sink. */
+typedef int (*rpq_pairs_sink)(const uint32_t *src, const uint32_t *dst, uint64_t n, void *ctx);
+rpq_status rpq_eval_allpairs_stream(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
+                                    uint64_t device_budget_bytes, uint64_t piece_pairs,
+                                    rpq_pairs_sink sink, void *ctx, uint64_t *total);
+
 /* ------------------------------------------------------------------------
  * CRPQ (Definition 2): all homomorphisms f: V_q -> V with
  * (1) L(f(u)) = L_q(u) where a label is given, (2) (f(x), f(y)) in R(rho) for

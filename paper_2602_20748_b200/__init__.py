@@ -111,7 +111,7 @@ EXPORTED = [
     "crpq_eval", "rpq_result_count", "rpq_result_device_view", "rpq_result_copy_host",
     "rpq_result_source_counts", "rpq_result_stats", "rpq_result_free", "rpq_last_error",
     "rpq_device_count", "rpq_version", "rpq_shard_plan", "rpq_trim_memory",
-    "rpq_nfa_reverse", "rpq_eval_targets", "rpq_eval_single_target",
+    "rpq_nfa_reverse", "rpq_eval_targets", "rpq_eval_single_target", "rpq_eval_allpairs_stream",
 ]
 
 _c = {}
@@ -131,6 +131,10 @@ _c["rpq_nfa_reverse"] = _proto("rpq_nfa_reverse", _st, [_vp, _P(_vp)])
 _c["rpq_eval_allpairs"] = _proto("rpq_eval_allpairs", _st, [_vp, _vp, _P(rpq_eval_opts), _P(_vp)])
 _c["rpq_eval_single_source"] = _proto("rpq_eval_single_source", _st, [_vp, _vp, ctypes.c_uint32,
                                                                       _P(rpq_eval_opts), _P(_vp)])
+RPQ_PAIRS_SINK = ctypes.CFUNCTYPE(ctypes.c_int, c_u32p, c_u32p, ctypes.c_uint64, ctypes.c_void_p)
+_c["rpq_eval_allpairs_stream"] = _proto("rpq_eval_allpairs_stream", _st,
+                                        [_vp, _vp, _P(rpq_eval_opts), ctypes.c_uint64, ctypes.c_uint64,
+                                         RPQ_PAIRS_SINK, ctypes.c_void_p, _P(ctypes.c_uint64)])
 _c["rpq_eval_targets"] = _proto("rpq_eval_targets", _st, [_vp, _vp, c_u32p, ctypes.c_uint64,
                                                           _P(rpq_eval_opts), _P(_vp)])
 _c["rpq_eval_single_target"] = _proto("rpq_eval_single_target", _st, [_vp, _vp, ctypes.c_uint32,
@@ -405,6 +409,32 @@ def rpq_eval_sources(g: Graph, a: Nfa, sources, opts: Optional[rpq_eval_opts] = 
     _check(_c["rpq_eval_sources"](g.h, a.h, _ptr(s, ctypes.c_uint32), len(sources), ctypes.byref(o),
                                   ctypes.byref(h)))
     return Result(h.value)
+
+
+def rpq_eval_allpairs_stream(g: Graph, a: Nfa, sink=None, device_budget_bytes: int = 0, piece_pairs: int = 0,
+                             opts: Optional[rpq_eval_opts] = None, **kw):
+    """All-pairs result streamed to the host in (src, dst) order.  sink(src,
+    dst) receives numpy views valid during the call (return True to stop);
+    without a sink the pieces are collected and returned as an (n, 2) array.
+    Returns (total pairs delivered, collected array or None)."""
+    o = opts if opts is not None else make_opts(**kw)
+    pieces = []
+
+    def _cb(ps, pd, n, _ctx):
+        src = np.ctypeslib.as_array(ps, (n,)) if n else np.zeros(0, np.uint32)
+        dst = np.ctypeslib.as_array(pd, (n,)) if n else np.zeros(0, np.uint32)
+        if sink is None:
+            pieces.append(np.stack([src.copy(), dst.copy()], 1))
+            return 0
+        return 1 if sink(src, dst) else 0
+
+    cb = RPQ_PAIRS_SINK(_cb)
+    tot = ctypes.c_uint64()
+    _check(_c["rpq_eval_allpairs_stream"](g.h, a.h, ctypes.byref(o), int(device_budget_bytes), int(piece_pairs), cb,
+                                          None, ctypes.byref(tot)))
+    if sink is None:
+        return tot.value, (np.concatenate(pieces) if pieces else np.zeros((0, 2), np.uint32))
+    return tot.value, None
 
 
 def rpq_eval_targets(g: Graph, a: Nfa, targets, opts: Optional[rpq_eval_opts] = None, **kw) -> Result:

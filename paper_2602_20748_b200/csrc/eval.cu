@@ -1268,6 +1268,11 @@ __global__ void k_clear_dense(uint64_t *Vis, uint64_t *Done, uint64_t words, uin
     for (uint64_t i = i0; i < ntu; i += st) TU[i] = 0;
 }
 
+__global__ void k_add_const(uint32_t *x, uint64_t n, uint32_t c) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+        x[j] += c;
+}
+
 __global__ void k_iota(uint32_t *x, uint64_t n) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
         x[j] = (uint32_t)j;
@@ -2600,6 +2605,108 @@ extern "C" rpq_status rpq_eval_sources(const rpq_graph *g, const rpq_nfa *a, con
     st = eval_sources_device(g, a, d, n, opts, out);
     dev_free(d, s);
     return st;
+}
+
+extern "C" rpq_status rpq_eval_allpairs_stream(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
+                                               uint64_t device_budget_bytes, uint64_t piece_pairs,
+                                               rpq_pairs_sink sink, void *ctx, uint64_t *total) {
+    if (total) *total = 0;
+    rpq_result *dummy = nullptr;
+    rpq_status st = check_common(g, a, &dummy);
+    if (st) return st;
+    if (!sink) return rpq_fail(RPQ_EINVAL, "rpq_eval_allpairs_stream: NULL sink");
+    rpq_eval_opts o{};
+    if (opts) o = *opts;
+    const uint32_t shard_count = o.shard_count ? o.shard_count : 1;
+    if (o.shard_index >= shard_count) return rpq_fail(RPQ_EINVAL, "shard_index >= shard_count");
+    RPQ_CUDA_TRY(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)o.cuda_stream;
+    if (!piece_pairs) piece_pairs = 1ull << 26;
+    // (1) output size per source: one PER_SOURCE pass over all of V
+    rpq_eval_opts po = o;
+    po.mode = RPQ_PER_SOURCE;
+    po.shard_index = 0;
+    po.shard_count = 1;
+    rpq_result *pr = nullptr;
+    if ((st = eval_sources_device(g, a, nullptr, 0, &po, &pr)) != RPQ_OK) return st;
+    std::vector<uint32_t> ps(pr->n_ps);
+    std::vector<uint64_t> pc(pr->n_ps);
+    if (pr->n_ps) {
+        cudaMemcpy(ps.data(), pr->ps_src, pr->n_ps * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(pc.data(), pr->ps_cnt, pr->n_ps * 8, cudaMemcpyDeviceToHost);
+    }
+    rpq_result_release(pr);
+    RPQ_CUDA_TRY(cudaGetLastError());
+    // (2) chunks of consecutive sources whose pairs fit the device budget
+    if (!device_budget_bytes) device_budget_bytes = dev_available() / 4;
+    const uint64_t cap = std::max<uint64_t>(device_budget_bytes / 8, 1);
+    std::vector<uint32_t> cstart{0};
+    uint64_t acc = 0;
+    for (size_t i = 0; i < ps.size(); ++i) {
+        if (acc && acc + pc[i] > cap) { cstart.push_back(ps[i]); acc = 0; }
+        acc += pc[i];
+    }
+    cstart.push_back(g->nv);
+    // (3) per chunk: PAIRS on the device, pieces through pinned buffers
+    uint32_t *h[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    struct Cleanup {
+        uint32_t *(*h)[2]; cudaStream_t *cs; cudaEvent_t *ev;
+        ~Cleanup() {
+            for (int b = 0; b < 2; ++b) for (int c = 0; c < 2; ++c) if (h[b][c]) cudaFreeHost(h[b][c]);
+            for (int b = 0; b < 2; ++b) if (ev[b]) cudaEventDestroy(ev[b]);
+            if (*cs) cudaStreamDestroy(*cs);
+        }
+    } cl{h, &cs, ev};
+    for (int b = 0; b < 2; ++b)
+        for (int c = 0; c < 2; ++c) RPQ_CUDA_TRY(cudaMallocHost(&h[b][c], piece_pairs * 4));
+    RPQ_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) RPQ_CUDA_TRY(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    uint64_t delivered = 0;
+    rpq_eval_opts co = o;
+    co.mode = RPQ_PAIRS | (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS));
+    co.shard_index = 0;
+    co.shard_count = 1;
+    for (size_t c = 0; c + 1 < cstart.size(); ++c) {
+        if (c % shard_count != o.shard_index) continue;
+        const uint32_t v0 = cstart[c], v1 = cstart[c + 1];
+        uint32_t *d = (uint32_t *)dev_alloc((uint64_t)(v1 - v0) * 4, s);
+        if (!d) return rpq_fail(RPQ_ENOMEM, "out of device memory (stream chunk)");
+        k_iota<<<grid_for(v1 - v0), 256, 0, s>>>(d, v1 - v0);
+        k_add_const<<<grid_for(v1 - v0), 256, 0, s>>>(d, v1 - v0, v0);
+        rpq_result *r = nullptr;
+        st = eval_sources_device(g, a, d, v1 - v0, &co, &r);
+        dev_free(d, s);
+        if (st != RPQ_OK) return st;
+        struct RG { rpq_result *r; ~RG() { rpq_result_release(r); } } rg{r};
+        const uint64_t n = r->nrows;
+        const uint64_t npieces = (n + piece_pairs - 1) / piece_pairs;
+        auto issue = [&](uint64_t k) -> cudaError_t {
+            const uint64_t o0 = k * piece_pairs, m = std::min<uint64_t>(piece_pairs, n - o0);
+            const int b = (int)(k & 1);
+            cudaError_t e = cudaMemcpyAsync(h[b][0], r->cols[0] + o0, m * 4, cudaMemcpyDeviceToHost, cs);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(h[b][1], r->cols[1] + o0, m * 4, cudaMemcpyDeviceToHost, cs);
+            if (e == cudaSuccess) e = cudaEventRecord(ev[b], cs);
+            return e;
+        };
+        if (npieces) RPQ_CUDA_TRY(issue(0));
+        for (uint64_t k = 0; k < npieces; ++k) {
+            const int b = (int)(k & 1);
+            RPQ_CUDA_TRY(cudaEventSynchronize(ev[b]));
+            if (k + 1 < npieces) RPQ_CUDA_TRY(issue(k + 1));   // overlaps the sink below
+            const uint64_t m = std::min<uint64_t>(piece_pairs, n - k * piece_pairs);
+            const int stop = sink(h[b][0], h[b][1], m, ctx);
+            delivered += m;
+            if (stop) {
+                cudaStreamSynchronize(cs);
+                if (total) *total = delivered;
+                return RPQ_OK;
+            }
+        }
+    }
+    if (total) *total = delivered;
+    return RPQ_OK;
 }
 
 extern "C" rpq_status rpq_eval_targets(const rpq_graph *g, const rpq_nfa *a, const uint32_t *targets,
