@@ -289,6 +289,15 @@ const char *rpq_version(void);
  * pool to the driver (e.g. before handing HBM to another allocator).
  * RPQ_EINVAL if device is not a CUDA device; RPQ_ECUDA on driver errors. */
 rpq_status rpq_trim_memory(int device);
+/* Replace the pool by the caller's device allocator (e.g. a framework's
+ * caching allocator): alloc(bytes, stream, ctx) returns device memory usable
+ * in stream order on `stream` (NULL on failure -> RPQ_ENOMEM), free_(ptr,
+ * stream, ctx) releases it.  Both NULL restores the pool.  Set it before any
+ * graph/evaluation whose buffers it would free (results free their buffers
+ * through the allocator current at rpq_result_free).  Process-wide.
+ * EINVAL if exactly one of the two functions is NULL. */
+rpq_status rpq_set_allocator(void *(*alloc)(size_t bytes, void *stream, void *ctx),
+                             void (*free_)(void *ptr, void *stream, void *ctx), void *ctx);
 
 #ifdef __cplusplus
 }

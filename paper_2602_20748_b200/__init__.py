@@ -112,6 +112,7 @@ EXPORTED = [
     "rpq_result_source_counts", "rpq_result_stats", "rpq_result_free", "rpq_last_error",
     "rpq_device_count", "rpq_version", "rpq_shard_plan", "rpq_trim_memory",
     "rpq_nfa_reverse", "rpq_eval_targets", "rpq_eval_single_target", "rpq_eval_allpairs_stream",
+    "rpq_set_allocator",
 ]
 
 _c = {}
@@ -131,6 +132,9 @@ _c["rpq_nfa_reverse"] = _proto("rpq_nfa_reverse", _st, [_vp, _P(_vp)])
 _c["rpq_eval_allpairs"] = _proto("rpq_eval_allpairs", _st, [_vp, _vp, _P(rpq_eval_opts), _P(_vp)])
 _c["rpq_eval_single_source"] = _proto("rpq_eval_single_source", _st, [_vp, _vp, ctypes.c_uint32,
                                                                       _P(rpq_eval_opts), _P(_vp)])
+RPQ_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+RPQ_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+_c["rpq_set_allocator"] = _proto("rpq_set_allocator", _st, [RPQ_ALLOC_FN, RPQ_FREE_FN, ctypes.c_void_p])
 RPQ_PAIRS_SINK = ctypes.CFUNCTYPE(ctypes.c_int, c_u32p, c_u32p, ctypes.c_uint64, ctypes.c_void_p)
 _c["rpq_eval_allpairs_stream"] = _proto("rpq_eval_allpairs_stream", _st,
                                         [_vp, _vp, _P(rpq_eval_opts), ctypes.c_uint64, ctypes.c_uint64,
@@ -286,6 +290,25 @@ def rpq_device_count() -> int:
 
 def rpq_version() -> str:
     return _c["rpq_version"]().decode()
+
+
+_allocator_refs = None
+
+
+def rpq_set_allocator(alloc=None, free=None) -> None:
+    """alloc(nbytes, stream) -> device pointer (int), free(ptr, stream);
+    both None restores the library's stream-ordered pool.  Example (PyTorch's
+    caching allocator): alloc=lambda n, s: torch.cuda.caching_allocator_alloc(n, stream=s),
+    free=lambda p, s: torch.cuda.caching_allocator_delete(p)."""
+    global _allocator_refs
+    if alloc is None and free is None:
+        _check(_c["rpq_set_allocator"](RPQ_ALLOC_FN(), RPQ_FREE_FN(), None))
+        _allocator_refs = None
+        return
+    fa = RPQ_ALLOC_FN(lambda n, s, _ctx: alloc(int(n), s or 0) or None)
+    ff = RPQ_FREE_FN(lambda p, s, _ctx: free(p, s or 0))
+    _allocator_refs = (fa, ff)      # keep the thunks alive while installed
+    _check(_c["rpq_set_allocator"](fa, ff, None))
 
 
 def rpq_trim_memory(device: int = 0) -> None:

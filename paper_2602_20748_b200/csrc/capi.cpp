@@ -43,8 +43,37 @@ extern "C" rpq_status rpq_device_count(int *n) {
 // recycled without cudaMalloc/cudaFree page-mapping costs.
 static std::once_flag g_pool_once[64];
 
+// optional caller allocator (rpq_set_allocator), e.g. a framework's caching
+// allocator; replaces the pool for every device allocation of the library
+namespace {
+struct UserAlloc {
+    void *(*alloc)(size_t, void *, void *) = nullptr;
+    void (*free_)(void *, void *, void *) = nullptr;
+    void *ctx = nullptr;
+};
+std::mutex g_ua_mu;
+UserAlloc g_ua;
+UserAlloc user_alloc() {
+    std::lock_guard<std::mutex> lk(g_ua_mu);
+    return g_ua;
+}
+}  // namespace
+
+extern "C" rpq_status rpq_set_allocator(void *(*alloc)(size_t bytes, void *stream, void *ctx),
+                                        void (*free_)(void *ptr, void *stream, void *ctx), void *ctx) {
+    if ((alloc == nullptr) != (free_ == nullptr))
+        return rpq_fail(RPQ_EINVAL, "rpq_set_allocator: give both functions or neither");
+    std::lock_guard<std::mutex> lk(g_ua_mu);
+    g_ua.alloc = alloc;
+    g_ua.free_ = free_;
+    g_ua.ctx = ctx;
+    return RPQ_OK;
+}
+
 void *dev_alloc(size_t bytes, void *stream) {
     if (bytes == 0) bytes = 16;
+    const UserAlloc ua = user_alloc();
+    if (ua.alloc) return ua.alloc(bytes, stream, ua.ctx);
     int dev = 0;
     cudaGetDevice(&dev);
     std::call_once(g_pool_once[dev & 63], [dev]() {
@@ -125,7 +154,10 @@ extern "C" rpq_status rpq_trim_memory(int device) {
 }
 
 void dev_free(void *p, void *stream) {
-    if (p) cudaFreeAsync(p, (cudaStream_t)stream);
+    if (!p) return;
+    const UserAlloc ua = user_alloc();
+    if (ua.free_) ua.free_(p, stream, ua.ctx);
+    else cudaFreeAsync(p, (cudaStream_t)stream);
 }
 
 // ---- automaton -----------------------------------------------------------
