@@ -132,8 +132,10 @@ def algorithmic_bytes(st):
     transition) CSR offset pair, 4 B per (row-group, edge) neighbour id, 16 B
     per (non-zero frontier word, edge) operation (visited read 8 B + the OR of
     the new bits into it 8 B -- SURVEY.md §8(d)'s "Vis read + Next RMW")."""
+    # bottom-up levels (symmetric labels, DESIGN.md): 8 B per in-neighbour
+    # visited-word load and 8 B per scanned target word
     return (24 * st["word_items"] + 8 * st["item_transitions"] + 4 * st["item_edges"]
-            + 16 * st["word_edge_ops"])
+            + 16 * st["word_edge_ops"] + 8 * st.get("pull_loads", 0) + 8 * st.get("pull_words", 0))
 
 
 # --------------------------------------------------------------------------
@@ -335,6 +337,25 @@ def run_ours(args):
         "gpu_launches": agg["launches"],
         "clocks": clk.summary(),
     }
+    if world == 1 and args.workload != "cfg5":
+        # PAIRS mode (timed separately from the COUNT headline):
+        # sorted distinct pairs materialised in device memory, per query
+        pr = {}
+        for rx in queries:
+            a = R.rpq_compile(G, rx)
+            R.rpq_eval_allpairs(G, a, mode=R.RPQ_PAIRS, stream=sp)          # warm-up (pool growth)
+            ts = []
+            for _ in range(3):
+                torch.cuda.synchronize()
+                ev0.record(stream)
+                r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_PAIRS, stream=sp)
+                ev1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(ev0.elapsed_time(ev1))
+                n = r.count
+                del r
+            pr[rx] = {"pairs": n, "ms": statistics.median(ts), "pairs_per_s": n / (statistics.median(ts) / 1e3)}
+        line["pairs_mode"] = {"unit": "pairs/s", "device_resident": True, "queries": pr}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, g, queries, budget_s=args.cpu_seconds)
     print(json.dumps(line), flush=True)
