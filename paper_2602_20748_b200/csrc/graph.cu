@@ -49,12 +49,27 @@ __global__ void k_scatter(const uint32_t *src, const uint32_t *dst, const uint16
     }
 }
 
-__global__ void k_degree_nbr(const uint64_t *keys, uint64_t m, uint32_t *deg, uint32_t *nbr) {
+// The unique-edge count m of the label stays on the device (no host round
+// trip per label): the kernels read it.
+__global__ void k_degree_nbr(const uint64_t *keys, const uint64_t *m_dev, uint32_t *deg, uint32_t *nbr,
+                             uint32_t *mm, uint64_t *fl) {
+    const uint64_t m = *m_dev;
+    uint32_t lo = 0xffffffffu, hi = 0u;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
         uint64_t k = keys[i];
-        nbr[i] = (uint32_t)k;
+        const uint32_t w = (uint32_t)k;
+        nbr[i] = w;
         atomicAdd(&deg[(k >> 32) + 1], 1u);
+        lo = min(lo, w);
+        hi = max(hi, w);
     }
+    // destination range (reduced per warp, then one atomic per warp)
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) { atomicMin(mm, lo); atomicMax(mm + 1, hi); }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && m) { fl[0] = keys[0]; fl[1] = keys[m - 1]; }   // source range
 }
 
 inline int grid_for(uint64_t n, int block = 256) {
@@ -75,8 +90,10 @@ struct Cleanup {
 extern "C" void rpq_graph_free(rpq_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
-    for (auto &c : g->csr) { cudaFree(c.off); cudaFree(c.nbr); }
-    for (auto &c : g->in_csr) { cudaFree(c.off); cudaFree(c.nbr); }
+    for (int p = 0; p < 2; ++p) {    // label CSRs are slices of these blocks
+        if (g->off_base[p]) cudaFree(g->off_base[p]);
+        if (g->nbr_base[p]) cudaFree(g->nbr_base[p]);
+    }
     if (g->vlabel) cudaFree(g->vlabel);
     delete g;
     dev_available_invalidate();
@@ -143,69 +160,82 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
     auto fail = [&](rpq_status st, const char *m) { rpq_graph_free(g); return rpq_fail(st, "rpq_graph_load: %s", m); };
 
     // pass 0: out-edge CSR (keys u<<32|w); pass 1 (RPQ_GRAPH_IN_EDGES): the
-    // in-edge CSR of the transposed graph (keys w<<32|u), same construction
-    for (int pass = 0; pass < (in_edges ? 2 : 1); ++pass) {
-    RPQ_CUDA_TRY(cudaMemcpyAsync(d_cnt, start.data(), nl * 8ull, cudaMemcpyHostToDevice, s));
-    if (ne) {
-        if (pass == 0) k_scatter<<<grid_for(ne), 256, 0, s>>>(d_src, d_dst, d_lab, ne, d_cnt, keys);
-        else k_scatter<<<grid_for(ne), 256, 0, s>>>(d_dst, d_src, d_lab, ne, d_cnt, keys);
-    }
-    RPQ_CUDA_TRY(cudaGetLastError());
-    std::vector<LabelCSR> &csrs = pass == 0 ? g->csr : g->in_csr;
+    // in-edge CSR of the transposed graph (keys w<<32|u), same construction.
+    // One allocation for all labels' offsets and one for all neighbour
+    // arrays (label slices 16-byte aligned, sized by the pre-dedup counts);
+    // per-label results stay on the device and are read back once per pass.
+    std::vector<uint64_t> nstart(nl + 1, 0);
+    for (uint32_t l = 0; l < nl; ++l) nstart[l + 1] = nstart[l] + ((cnt[l] + 3) / 4) * 4;
+    uint64_t *d_m = (uint64_t *)alloc(nl * 8ull), *d_fl = (uint64_t *)alloc(nl * 16ull);
+    uint32_t *d_mm = (uint32_t *)alloc(nl * 8ull);
+    if (!d_m || !d_fl || !d_mm) return fail(RPQ_ENOMEM, "out of device memory");
+    // CUB temporary storage: the largest need over the labels, allocated once
+    size_t tbytes = 0;
     for (uint32_t l = 0; l < nl; ++l) {
-        LabelCSR &c = csrs[l];
-        uint64_t n = cnt[l];
-        c.off = nullptr;
-        if (cudaMalloc(&c.off, (nv + 1ull) * 4) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "CSR offsets"); }
-        RPQ_CUDA_TRY(cudaMemsetAsync(c.off, 0, (nv + 1ull) * 4, s));
-        if (n == 0) {
-            if (cudaMalloc(&c.nbr, 16) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "CSR"); }
-            continue;
-        }
-        uint64_t *kin = keys + start[l], *kout = keys2 + start[l];
-        size_t tbytes = 0, t2 = 0, t3 = 0;
-        cub::DeviceRadixSort::SortKeys(nullptr, tbytes, kin, kout, (int64_t)n, 0, 32 + vbits, s);
-        cub::DeviceSelect::Unique(nullptr, t2, kout, kin, d_nsel, (int64_t)n, s);
-        tbytes = std::max(tbytes, t2);
-        void *tstore = dev_alloc(tbytes, s);
-        if (!tstore) return fail(RPQ_ENOMEM, "sort temp");
-        cub::DeviceRadixSort::SortKeys(tstore, tbytes, kin, kout, (int64_t)n, 0, 32 + vbits, s);
-        cub::DeviceSelect::Unique(tstore, tbytes, kout, kin, d_nsel, (int64_t)n, s);
-        dev_free(tstore, s);
-        uint64_t m = 0;
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&m, d_nsel, 8, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        c.m = m;
-        if (cudaMalloc(&c.nbr, std::max<uint64_t>(m, 4) * 4) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "CSR nbr"); }
-        k_degree_nbr<<<grid_for(m), 256, 0, s>>>(kin, m, c.off, c.nbr);
-        cub::DeviceScan::InclusiveSum(nullptr, t3, c.off, c.off, (int64_t)nv + 1, s);
-        void *ts = dev_alloc(t3, s);
-        if (!ts) return fail(RPQ_ENOMEM, "scan temp");
-        cub::DeviceScan::InclusiveSum(ts, t3, c.off, c.off, (int64_t)nv + 1, s);
-        dev_free(ts, s);
-        // source range from the sorted keys, destination range by reduction
-        uint64_t kfirst = 0, klast = 0;
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&kfirst, kin, 8, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&klast, kin + m - 1, 8, cudaMemcpyDeviceToHost, s));
-        uint32_t *d_mm = (uint32_t *)dev_alloc(8, s);
-        size_t t4 = 0, t5 = 0;
-        cub::DeviceReduce::Min(nullptr, t4, c.nbr, d_mm, (int64_t)m, s);
-        cub::DeviceReduce::Max(nullptr, t5, c.nbr, d_mm + 1, (int64_t)m, s);
-        void *tr = dev_alloc(std::max(t4, t5), s);
-        if (!d_mm || !tr) return fail(RPQ_ENOMEM, "reduce temp");
-        cub::DeviceReduce::Min(tr, t4, c.nbr, d_mm, (int64_t)m, s);
-        cub::DeviceReduce::Max(tr, t5, c.nbr, d_mm + 1, (int64_t)m, s);
-        uint32_t mm[2];
-        RPQ_CUDA_TRY(cudaMemcpyAsync(mm, d_mm, 8, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        dev_free(tr, s);
-        dev_free(d_mm, s);
-        c.src_min = (uint32_t)(kfirst >> 32);
-        c.src_max = (uint32_t)(klast >> 32);
-        c.dst_min = mm[0];
-        c.dst_max = mm[1];
-        if (pass == 0) g->ne += m;
+        if (!cnt[l]) continue;
+        size_t t1 = 0, t2 = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, t1, keys, keys2, (int64_t)cnt[l], 0, 32 + vbits, s);
+        cub::DeviceSelect::Unique(nullptr, t2, keys2, keys, d_m, (int64_t)cnt[l], s);
+        tbytes = std::max(tbytes, std::max(t1, t2));
     }
+    {
+        size_t t3 = 0;
+        cub::DeviceScan::InclusiveSum(nullptr, t3, (uint32_t *)nullptr, (uint32_t *)nullptr, (int64_t)nv + 1, s);
+        tbytes = std::max(tbytes, t3);
+    }
+    void *tstore = alloc(std::max<size_t>(tbytes, 16));
+    if (!tstore) return fail(RPQ_ENOMEM, "sort temp");
+    for (int pass = 0; pass < (in_edges ? 2 : 1); ++pass) {
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_cnt, start.data(), nl * 8ull, cudaMemcpyHostToDevice, s));
+        if (ne) {
+            if (pass == 0) k_scatter<<<grid_for(ne), 256, 0, s>>>(d_src, d_dst, d_lab, ne, d_cnt, keys);
+            else k_scatter<<<grid_for(ne), 256, 0, s>>>(d_dst, d_src, d_lab, ne, d_cnt, keys);
+        }
+        RPQ_CUDA_TRY(cudaGetLastError());
+        std::vector<LabelCSR> &csrs = pass == 0 ? g->csr : g->in_csr;
+        uint32_t *&off_all = g->off_base[pass];
+        uint32_t *&nbr_all = g->nbr_base[pass];
+        if (cudaMalloc(&off_all, (uint64_t)nl * (nv + 1ull) * 4) != cudaSuccess ||
+            cudaMalloc(&nbr_all, std::max<uint64_t>(nstart[nl], 4) * 4) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(RPQ_ENOMEM, "CSR arrays");
+        }
+        RPQ_CUDA_TRY(cudaMemsetAsync(off_all, 0, (uint64_t)nl * (nv + 1ull) * 4, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(d_m, 0, nl * 8ull, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(d_fl, 0, nl * 16ull, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(d_mm, 0xff, nl * 8ull, s));   // (min, max) = (~0, ~0): max fixed below
+        for (uint32_t l = 0; l < nl; ++l) {
+            LabelCSR &c = csrs[l];
+            c.off = off_all + (uint64_t)l * (nv + 1ull);
+            c.nbr = nbr_all + nstart[l];
+            const uint64_t n = cnt[l];
+            if (n == 0) continue;
+            uint64_t *kin = keys + start[l], *kout = keys2 + start[l];
+            size_t tb = tbytes;
+            RPQ_CUDA_TRY(cudaMemsetAsync(d_mm + 2 * l + 1, 0, 4, s));
+            cub::DeviceRadixSort::SortKeys(tstore, tb, kin, kout, (int64_t)n, 0, 32 + vbits, s);
+            tb = tbytes;
+            cub::DeviceSelect::Unique(tstore, tb, kout, kin, d_m + l, (int64_t)n, s);
+            k_degree_nbr<<<grid_for(n), 256, 0, s>>>(kin, d_m + l, c.off, c.nbr, d_mm + 2 * l, d_fl + 2 * l);
+            tb = tbytes;
+            cub::DeviceScan::InclusiveSum(tstore, tb, c.off, c.off, (int64_t)nv + 1, s);
+        }
+        std::vector<uint64_t> hm(nl), hfl(2 * nl);
+        std::vector<uint32_t> hmm(2 * nl);
+        RPQ_CUDA_TRY(cudaMemcpyAsync(hm.data(), d_m, nl * 8ull, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(hfl.data(), d_fl, nl * 16ull, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(hmm.data(), d_mm, nl * 8ull, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        for (uint32_t l = 0; l < nl; ++l) {
+            LabelCSR &c = csrs[l];
+            c.m = cnt[l] ? hm[l] : 0;
+            if (!c.m) continue;              // empty label: min > max (defaults)
+            c.src_min = (uint32_t)(hfl[2 * l] >> 32);
+            c.src_max = (uint32_t)(hfl[2 * l + 1] >> 32);
+            c.dst_min = hmm[2 * l];
+            c.dst_max = hmm[2 * l + 1];
+            if (pass == 0) g->ne += c.m;
+        }
     }
     if (d->vertex_label) {
         if (d->num_vertex_labels && d->vertex_label_names)

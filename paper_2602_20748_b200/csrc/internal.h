@@ -31,6 +31,8 @@ struct rpq_graph {
     std::vector<std::string> vlabel_names;
     std::vector<LabelCSR> csr;   // [num_labels]
     std::vector<LabelCSR> in_csr;   // [num_labels] in-edges (RPQ_GRAPH_IN_EDGES), else empty
+    uint32_t *off_base[2] = {nullptr, nullptr};   // [out/in] all labels' offsets (one block)
+    uint32_t *nbr_base[2] = {nullptr, nullptr};   // [out/in] all labels' neighbours (one block)
     uint16_t *vlabel = nullptr;  // device [nv] or null
     std::vector<uint16_t> h_vlabel;   // host copy (CRPQ planning)
     // per label: is the edge set symmetric ((u,l,w) in E <=> (w,l,u) in E)?
