@@ -320,6 +320,8 @@ def run_ours(args):
                              f"batches of shards 0..{world - 1} of {nshard} (1/{sample} of the all-pairs query)"},
         "roofline": {"bound": "hbm", "kernel": "k_level (level loop: k_units + k_level + k_level_hub)",
                      "achieved": achieved, "peak": peak,
+                     "peak_nominal": 8000.0,
+                     "frac_nominal": (achieved / 8000.0) if achieved else None,
                      "peak_source": peak_src, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
                      "algorithmic_bytes_per_launch": per_launch,
@@ -364,12 +366,24 @@ def run_ours(args):
 
 
 # --------------------------------------------------------------------------
-def oracle_sample(g, queries, budget_s, seed=0):
-    """Time the oracle (O1, all host threads) on seeded source samples of the
-    workload, growing the sample until ~budget_s seconds of CPU work."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_sample(g, queries, budget_s, seed=0, threads=0):
+    """Time the oracle (O1, all host threads unless `threads`) on seeded
+    source samples of the workload, growing the sample until ~budget_s
+    seconds of CPU work."""
     import oracle
     og = oracle.OracleGraph(g)
-    threads = os.cpu_count() or 1
+    threads = threads or os.cpu_count() or 1
     rng = np.random.default_rng(seed)
     order = rng.permutation(g.num_vertices).astype(np.uint32)
     n, pe, secs, used = 64, 0, 0.0, 0
@@ -387,7 +401,9 @@ def oracle_sample(g, queries, budget_s, seed=0):
 
 def cpu_baseline(args, g, queries, budget_s):
     pe, secs, used, threads = oracle_sample(g, queries, budget_s)
+    pe1, secs1, _, _ = oracle_sample(g, queries, min(4.0, budget_s / 4), seed=7, threads=1)
     return {"value": pe / secs, "unit": "PE/s", "cores": threads, "kind": "oracle",
+            "cpu_model": cpu_model(), "single_thread_value": pe1 / secs1,
             "sample": f"{used} seeded random sources x {len(queries)} queries of {args.workload} "
                       f"({pe:.3e} PE in {secs:.1f} s)"}
 
