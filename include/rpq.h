@@ -251,6 +251,8 @@ typedef struct {
     uint64_t pull_levels;       /* levels run bottom-up (direction-optimising), over batches */
     uint64_t pull_loads;        /* in-neighbour visited-word loads of the pull levels */
     uint64_t pull_words;        /* (row, word) pairs scanned by the pull levels */
+    uint64_t adv_words;         /* words read by the top-down advance (Vis + Done of active chunks) */
+    uint64_t adv_zero_sectors;  /* ... 4-word sectors of those without frontier bits */
 } rpq_stats;
 
 uint64_t rpq_result_count(const rpq_result *r);

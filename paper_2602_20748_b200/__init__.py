@@ -85,7 +85,8 @@ class rpq_stats(ctypes.Structure):
                 ("state_words", ctypes.c_uint64), ("expand_launches", ctypes.c_uint64),
                 ("kernel_launches", ctypes.c_uint64), ("expand_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("pull_levels", ctypes.c_uint64),
-                ("pull_loads", ctypes.c_uint64), ("pull_words", ctypes.c_uint64)]
+                ("pull_loads", ctypes.c_uint64), ("pull_words", ctypes.c_uint64),
+                ("adv_words", ctypes.c_uint64), ("adv_zero_sectors", ctypes.c_uint64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -55,7 +55,7 @@ constexpr int MAXT = RPQ_MAX_TRANSITIONS;
 constexpr int MAXL = RPQ_MAX_QUERY_LABELS;
 constexpr uint32_t HUB_EDGES = 512;      // edges per hub segment
 constexpr int TILE_V = 1024;             // vertices per extraction tile
-constexpr int NSTAT = 12;
+constexpr int NSTAT = 14;
 #ifndef RPQ_LEVEL_MINB
 #define RPQ_LEVEL_MINB 5
 #endif
@@ -159,7 +159,7 @@ struct LevelArgs {
 
 // stats slots
 enum { S_PE = 0, S_WORD_ITEMS, S_WORD_EDGE, S_ITEMS, S_ITEM_EDGES, S_ITEM_TRANS, S_X_RED, S_N_RED, S_PULL_LEVELS,
-       S_PULL_LOADS, S_PULL_WORDS, S_PE_POST };
+       S_PULL_LOADS, S_PULL_WORDS, S_PE_POST, S_ADV_WORDS, S_ADV_ZERO_SECTORS };
 
 __device__ __forceinline__ uint64_t ld_cg(const uint64_t *p) { return __ldcg((const unsigned long long *)p); }
 
@@ -566,6 +566,20 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                         // sources of this frontier word may gain bits next level
                         if (p.pull_mode) act_or(actS, p.ActNext, (uint32_t)(rb - row * p.nw) + bt * p.cw, f[k]);
                         if (STATS) st[S_WORD_ITEMS]++;
+                    }
+                }
+                if constexpr (STATS) {   // advance reads vs 32-byte sectors without frontier bits
+#pragma unroll
+                    for (int k = 0; k < KGRP; ++k) {
+                        const uint32_t bt = (uint32_t)(bits >> (8 * k)) & 0xffu;
+                        const bool okk = k < nk && lane_ok && xw * 32u * p.cw + bt * p.cw + lane < p.nw;
+                        const unsigned vm = __ballot_sync(0xffffffffu, okk);
+                        const unsigned nzm = __ballot_sync(0xffffffffu, okk && f[k] != 0);
+                        if (lane == 0) {
+                            st[S_ADV_WORDS] += __popc(vm);
+                            for (int sct = 0; sct < 8; ++sct)
+                                if (((vm >> (4 * sct)) & 15u) && !((nzm >> (4 * sct)) & 15u)) st[S_ADV_ZERO_SECTORS]++;
+                        }
                     }
                 }
                 bool anyk = false;
@@ -2536,6 +2550,8 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         ST.pull_levels = hs[S_PULL_LEVELS];
         ST.pull_loads = hs[S_PULL_LOADS];
         ST.pull_words = hs[S_PULL_WORDS];
+        ST.adv_words = hs[S_ADV_WORDS];
+        ST.adv_zero_sectors = hs[S_ADV_ZERO_SECTORS];
         ST.word_items = hs[S_WORD_ITEMS];
         ST.word_edge_ops = hs[S_WORD_EDGE];
         ST.items = hs[S_ITEMS];

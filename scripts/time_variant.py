@@ -45,4 +45,6 @@ for rx in qs:
     sp = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=s.cuda_stream, shard_count=shards).stats()
     print(f"{tag:28s} {rx:10s} total_ms={best[0]:9.2f} loop_ms={best[1]:9.2f} count={best[2]} "
           f"PE={sp['product_edges']:.4e} pull_levels={sp['pull_levels']} levels={sp['levels']} "
-          f"pull_loads={sp['pull_loads']:.3e} pull_words={sp['pull_words']:.3e}", flush=True)
+          f"pull_loads={sp['pull_loads']:.3e} pull_words={sp['pull_words']:.3e} adv_words={sp['adv_words']:.3e} "
+          f"adv_zero_sectors={sp['adv_zero_sectors']:.3e} word_items={sp['word_items']:.3e} wordops={sp['word_edge_ops']:.3e}",
+          flush=True)
