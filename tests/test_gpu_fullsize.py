@@ -142,3 +142,50 @@ def test_cfg5_rmat24_sampled():
     pick = synth.sample_sources(s.size, 48, seed=24)
     o = oracle.eval_sources(og, rx, s[pick].astype(np.uint32), pairs=False, threads=os.cpu_count() or 1)
     assert np.array_equal(o["counts"], c[pick])
+
+
+def test_cfg2_stream_full_size_sampled():
+    """The streamed all-pairs output at BASELINE cfg2 size: all
+    7.95e9 pairs of a* reach the host in (src, dst) order; the pairs of a
+    seeded source sample are checked against O1 and the per-source counts of
+    every source against the device PER_SOURCE result."""
+    g = synth.uniform_graph()
+    G = R.rpq_graph_load(g)
+    a = R.rpq_compile(G, "a*")
+    sample = synth.sample_sources(g.num_vertices, 48, seed=77)
+    sset = set(sample.tolist())
+    per = np.zeros(g.num_vertices, np.uint64)
+    kept = []
+    last = [-1, -1]
+
+    npiece = [0]
+
+    def sink(src, dst):
+        # (src, dst) strictly increasing: across pieces always, within every
+        # 8th piece fully (the check is costly at 64 M pairs per piece)
+        if npiece[0] % 8 == 0:
+            inc = (src[1:] > src[:-1]) | ((src[1:] == src[:-1]) & (dst[1:] > dst[:-1]))
+            assert inc.all()
+        if last[0] >= 0:
+            assert (int(src[0]), int(dst[0])) > (last[0], last[1])
+        last[0], last[1] = int(src[-1]), int(dst[-1])
+        npiece[0] += 1
+        per[:] += np.bincount(src, minlength=g.num_vertices).astype(np.uint64)
+        lo = np.searchsorted(src, sample, "left")
+        hi = np.searchsorted(src, sample, "right")
+        for a0, b0 in zip(lo, hi):
+            if b0 > a0:
+                kept.append(np.stack([src[a0:b0], dst[a0:b0]], 1).copy())
+        return False
+
+    tot, _ = R.rpq_eval_allpairs_stream(G, a, sink=sink, device_budget_bytes=16 << 30)
+    s, c = R.rpq_eval_allpairs(G, a, mode=R.RPQ_PER_SOURCE).source_counts()
+    want_per = np.zeros(g.num_vertices, np.uint64)
+    want_per[s] = c
+    assert tot == int(want_per.sum()) and np.array_equal(per, want_per)
+    og = oracle.OracleGraph(g)
+    o = oracle.eval_sources(og, "a*", sample)
+    want = np.stack([o["src"], o["dst"]], 1).astype(np.uint32)
+    want = want[np.lexsort((want[:, 1], want[:, 0]))]
+    got = np.concatenate(kept).astype(np.uint32)
+    assert np.array_equal(got, want) and len(sset) == 48
