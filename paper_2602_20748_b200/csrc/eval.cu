@@ -116,6 +116,7 @@ struct Ctrl {                  // per-level device counters / flags
     uint32_t ucur[2];          // work-unit cursor (dynamic fetch) per parity
     uint32_t ntouched;         // entries of LevelArgs::TL
     uint32_t pcur[2];          // pull-level task cursor per parity
+    uint32_t hcur;             // hub-record cursor (reset per level and before the seed hub launch)
     // adaptive direction: a pull level counts the chunk-words that needed bits
     // and those it completed; if fewer than half complete (directed graphs
     // where most sources never reach most vertices), the batch stays top-down
@@ -229,6 +230,7 @@ __global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
 
         p.ctrl->nhub_items = 0;
         p.ctrl->nhub_recs = 0;
+        p.ctrl->hcur = 0;
         p.ctrl->levels += 1;
     }
     if (p.pull_mode)   // the previous level's filter, free now: this level accumulates into it
@@ -651,7 +653,14 @@ __global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A
     const uint32_t n = min(p.ctrl->nhub_recs, p.hrec_cap);
     unsigned long long st[NSTAT] = {};
     bool act = false;
-    for (uint64_t it = wid; it < n; it += nwarps) {
+    (void)wid; (void)nwarps;
+    // records differ in cost (1-8 chunks x up to HUB_EDGES edges): fetched
+    // dynamically, one atomic per record
+    for (;;) {
+        uint32_t it = 0;
+        if (lane == 0) it = atomicAdd(&p.ctrl->hcur, 1u);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= n) break;
         const HubRec r = p.hrecs[it];
         if (r.end == r.beg) continue;
         const HubItem h = p.hitems[r.hitem];
@@ -885,6 +894,7 @@ __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const 
         ctrl->active[1] = 0;
         ctrl->nhub_items = 0;
         ctrl->nhub_recs = 0;
+        ctrl->hcur = 0;
         ctrl->ucnt[0] = ctrl->ucnt[1] = 0;
         ctrl->ucur[0] = ctrl->ucur[1] = 0;
         ctrl->ntouched = 0;
