@@ -1638,7 +1638,7 @@ struct LevelGraph {
 
 template <bool STATS>
 cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg, const LevelArgs &P0,
-                              const LevelArgs &P1, int grid, int hgrid, uint64_t nxbwords) {
+                              const LevelArgs &P1, int grid, int hgrid, uint64_t nxbwords, bool hub) {
     cudaError_t e;
     if ((e = cudaGraphCreate(&LG.g, 0)) != cudaSuccess) return e;
     cudaGraphConditionalHandle h;
@@ -1682,12 +1682,12 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
     if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r0)) != cudaSuccess) return e;
     if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a0)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a0)) != cudaSuccess) return e;
-    if ((e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
+    if (hub && (e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u1)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a1)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a1)) != cudaSuccess) return e;
-    if ((e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
+    if (hub && (e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_end, dim3(1), dim3(1), m1)) != cudaSuccess) return e;
     return cudaGraphInstantiate(&LG.exec, LG.g, 0);
 }
@@ -1696,7 +1696,7 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
 // one flag readback per level.
 rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &P0, const LevelArgs &P1, int grid,
                            int hgrid, uint64_t nxbwords, cudaStream_t s, bool stats, uint32_t *h_flag,
-                           rpq_stats *out_stats) {
+                           rpq_stats *out_stats, bool hub) {
     int par = 0;
     const int ugrid = (int)std::min<uint64_t>(148 * 4, (nxbwords + 255) / 256 + 1);
     for (;;) {
@@ -1706,11 +1706,11 @@ rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &
         if (stats) {
             k_level<true><<<grid, 256, 0, s>>>(A, Sg, P);
             if (P.pull_mode) k_pull<true><<<148 * 8, 256, 0, s>>>(A, Sg, P);
-            k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
+            if (hub) k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
         } else {
             k_level<false><<<grid, 256, 0, s>>>(A, Sg, P);
             if (P.pull_mode) k_pull<false><<<148 * 8, 256, 0, s>>>(A, Sg, P);
-            k_level_hub<false><<<hgrid, 256, 0, s>>>(A, Sg, P);
+            if (hub) k_level_hub<false><<<hgrid, 256, 0, s>>>(A, Sg, P);
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(h_flag, &P.ctrl->active[par ^ 1], 4, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
@@ -1810,6 +1810,10 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         A.inbr[k] = use_t ? TCSR[slot_label[k]].nbr : all_sym ? A.nbr[k] : nullptr;
     }
     const bool pull_avail = all_sym || use_t;
+    // the hub kernel only runs if some label of the query has rows longer
+    // than HUB_EDGES (RMAT); otherwise its launches are left out of the loop
+    bool need_hub = getenv("RPQ_ALWAYS_HUB") != nullptr;
+    for (size_t k = 0; k < slot_label.size(); ++k) need_hub |= CSR[slot_label[k]].max_deg > HUB_EDGES;
     {   // transitions grouped by target state
         uint32_t k = 0;
         for (uint32_t q2 = 0; q2 < a->nq; ++q2) {
@@ -2286,8 +2290,8 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     const int hgrid = 148 * RPQ_HUB_MINB;
     LevelGraph LG;
     if (nbatches && !sparse_done && !getenv("RPQ_HOST_LOOP")) {
-        cudaError_t ge = stats ? build_level_graph<true>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords)
-                               : build_level_graph<false>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords);
+        cudaError_t ge = stats ? build_level_graph<true>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub)
+                               : build_level_graph<false>(LG, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub);
         if (ge != cudaSuccess) {   // fall back to the host-driven loop
             cudaGetLastError();
             if (LG.exec) cudaGraphExecDestroy(LG.exec);
@@ -2385,12 +2389,12 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             const int sg = grid_for((uint64_t)nb * 32, 256, 148 * 8);
             if (stats) {
                 k_seed_expand<true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
-                k_level_hub<true><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
+                if (need_hub) k_level_hub<true><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
             } else {
                 k_seed_expand<false><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
-                k_level_hub<false><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
+                if (need_hub) k_level_hub<false><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
             }
-            ST.kernel_launches += 2;
+            ST.kernel_launches += need_hub ? 2 : 1;
         }
         PT.mark("seed");
         rpq_status st = RPQ_OK;
@@ -2402,7 +2406,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             cudaError_t ge = cudaGraphLaunch(LG.exec, s);
             if (ge != cudaSuccess) st = rpq_fail(RPQ_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(ge));
         } else {
-            st = run_levels_host(A, d_layout, P0, P1, lgrid, hgrid, xbwords, s, stats, h_cnt, &ST);
+            st = run_levels_host(A, d_layout, P0, P1, lgrid, hgrid, xbwords, s, stats, h_cnt, &ST, need_hub);
         }
         if (timeit) cudaEventRecord(tev.back().second, s);
         PT.mark("levels");
@@ -2547,7 +2551,8 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         RPQ_CUDA_TRY(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
         ST.levels = hc.levels;
-        if (LG.exec) ST.kernel_launches += 3ull * hc.levels + (hc.levels + 1) / 2;
+        if (LG.exec)
+            ST.kernel_launches += (2ull + (need_hub ? 1 : 0) + (P0.pull_mode ? 2 : 0)) * hc.levels + (hc.levels + 1) / 2;
         ST.expand_launches = 2ull * ST.levels;
     }
     if (stats) {

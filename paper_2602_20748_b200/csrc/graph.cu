@@ -72,6 +72,15 @@ __global__ void k_degree_nbr(const uint64_t *keys, const uint64_t *m_dev, uint32
     if (blockIdx.x == 0 && threadIdx.x == 0 && m) { fl[0] = keys[0]; fl[1] = keys[m - 1]; }   // source range
 }
 
+// largest row of a label: max over v of off[v + 1] - off[v]
+__global__ void k_max_deg(const uint32_t *off, uint32_t nv, uint32_t *out) {
+    uint32_t m = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < nv; v += (uint64_t)gridDim.x * blockDim.x)
+        m = max(m, off[v + 1] - off[v]);
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 inline int grid_for(uint64_t n, int block = 256) {
     uint64_t g = (n + block - 1) / block;
     if (g > 148ull * 32) g = 148ull * 32;
@@ -167,8 +176,8 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
     std::vector<uint64_t> nstart(nl + 1, 0);
     for (uint32_t l = 0; l < nl; ++l) nstart[l + 1] = nstart[l] + ((cnt[l] + 3) / 4) * 4;
     uint64_t *d_m = (uint64_t *)alloc(nl * 8ull), *d_fl = (uint64_t *)alloc(nl * 16ull);
-    uint32_t *d_mm = (uint32_t *)alloc(nl * 8ull);
-    if (!d_m || !d_fl || !d_mm) return fail(RPQ_ENOMEM, "out of device memory");
+    uint32_t *d_mm = (uint32_t *)alloc(nl * 8ull), *d_md = (uint32_t *)alloc(nl * 4ull);
+    if (!d_m || !d_fl || !d_mm || !d_md) return fail(RPQ_ENOMEM, "out of device memory");
     // CUB temporary storage: the largest need over the labels, allocated once
     size_t tbytes = 0;
     for (uint32_t l = 0; l < nl; ++l) {
@@ -204,6 +213,7 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
         RPQ_CUDA_TRY(cudaMemsetAsync(d_m, 0, nl * 8ull, s));
         RPQ_CUDA_TRY(cudaMemsetAsync(d_fl, 0, nl * 16ull, s));
         RPQ_CUDA_TRY(cudaMemsetAsync(d_mm, 0xff, nl * 8ull, s));   // (min, max) = (~0, ~0): max fixed below
+        RPQ_CUDA_TRY(cudaMemsetAsync(d_md, 0, nl * 4ull, s));
         for (uint32_t l = 0; l < nl; ++l) {
             LabelCSR &c = csrs[l];
             c.off = off_all + (uint64_t)l * (nv + 1ull);
@@ -219,9 +229,11 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
             k_degree_nbr<<<grid_for(n), 256, 0, s>>>(kin, d_m + l, c.off, c.nbr, d_mm + 2 * l, d_fl + 2 * l);
             tb = tbytes;
             cub::DeviceScan::InclusiveSum(tstore, tb, c.off, c.off, (int64_t)nv + 1, s);
+            k_max_deg<<<grid_for(nv), 256, 0, s>>>(c.off, nv, d_md + l);
         }
         std::vector<uint64_t> hm(nl), hfl(2 * nl);
-        std::vector<uint32_t> hmm(2 * nl);
+        std::vector<uint32_t> hmm(2 * nl), hmd(nl);
+        RPQ_CUDA_TRY(cudaMemcpyAsync(hmd.data(), d_md, nl * 4ull, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaMemcpyAsync(hm.data(), d_m, nl * 8ull, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaMemcpyAsync(hfl.data(), d_fl, nl * 16ull, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaMemcpyAsync(hmm.data(), d_mm, nl * 8ull, cudaMemcpyDeviceToHost, s));
@@ -229,6 +241,7 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
         for (uint32_t l = 0; l < nl; ++l) {
             LabelCSR &c = csrs[l];
             c.m = cnt[l] ? hm[l] : 0;
+            c.max_deg = c.m ? hmd[l] : 0;
             if (!c.m) continue;              // empty label: min > max (defaults)
             c.src_min = (uint32_t)(hfl[2 * l] >> 32);
             c.src_max = (uint32_t)(hfl[2 * l + 1] >> 32);

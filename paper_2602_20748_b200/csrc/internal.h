@@ -21,6 +21,7 @@ struct LabelCSR {
     uint64_t m = 0;              // distinct edges with this label
     uint32_t src_min = 1, src_max = 0;   // empty label: min > max
     uint32_t dst_min = 1, dst_max = 0;
+    uint32_t max_deg = 0;        // largest row (long rows go to the hub kernel)
 };
 
 struct rpq_graph {
