@@ -1297,6 +1297,19 @@ __global__ void k_add_const(uint32_t *x, uint64_t n, uint32_t c) {
         x[j] += c;
 }
 
+__global__ void k_sample_idx(uint32_t *idx, uint64_t ns, uint64_t np) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < ns; k += (uint64_t)gridDim.x * blockDim.x)
+        idx[k] = (uint32_t)(k * np / ns);
+}
+
+__global__ void k_prod_bounds(const uint64_t *d_np, const uint32_t *pidx, const uint32_t *cand, uint64_t *out) {
+    if (threadIdx.x) return;
+    const uint64_t np = *d_np;
+    out[0] = np;
+    out[1] = np ? cand[pidx[0]] : 0u;
+    out[2] = np ? cand[pidx[np - 1]] : 0u;
+}
+
 __global__ void k_iota(uint32_t *x, uint64_t n) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
         x[j] = (uint32_t)j;
@@ -1836,9 +1849,10 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     }
     uint8_t *flag = (uint8_t *)ws.get(std::max<uint64_t>(nsrc, 1));
     uint32_t *pidx = (uint32_t *)ws.get(std::max<uint64_t>(nsrc, 1) * 4);
-    uint64_t *d_np = (uint64_t *)ws.get(8);
+    uint64_t *d_np = (uint64_t *)ws.get(32);
     if (!flag || !pidx || !d_np) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
     uint64_t np = 0;
+    uint32_t p_first_d = 0, p_last_d = 0;
     if (nsrc && a->nq) {
         k_productive<<<grid_for(nsrc), 256, 0, s>>>(A, cand, nsrc, flag);
         ST.kernel_launches++;
@@ -1848,8 +1862,14 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         void *tmp = ws.get(tb);
         if (!tmp) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory"));
         cub::DeviceSelect::Flagged(tmp, tb, it, flag, pidx, d_np, (int64_t)nsrc, s);
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&np, d_np, 8, cudaMemcpyDeviceToHost, s));
+        // |P| and the first / last productive source in one readback
+        k_prod_bounds<<<1, 32, 0, s>>>(d_np, pidx, cand, d_np + 1);
+        uint64_t hb3[3] = {0, 0, 0};
+        RPQ_CUDA_TRY(cudaMemcpyAsync(hb3, d_np + 1, 24, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        np = hb3[0];
+        p_first_d = (uint32_t)hb3[1];
+        p_last_d = (uint32_t)hb3[2];
         HM("np readback");
     } else if (nsrc) {
         RPQ_CUDA_TRY(cudaMemsetAsync(flag, 0, nsrc, s));
@@ -1881,14 +1901,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     // ---- batch plan -------------------------------------------------------
     // Rows of the worst batch (q0 range = hull of all productive sources) set
     // the word budget: 3 state arrays x 8 B + worklists/bitmaps per word.
-    uint32_t p_first = 0, p_last = 0;
-    if (np) {
-        uint32_t j0 = 0, j1 = 0;
-        RPQ_CUDA_TRY(cudaMemcpy(&j0, pidx, 4, cudaMemcpyDeviceToHost));
-        RPQ_CUDA_TRY(cudaMemcpy(&j1, pidx + np - 1, 4, cudaMemcpyDeviceToHost));
-        RPQ_CUDA_TRY(cudaMemcpy(&p_first, cand + j0, 4, cudaMemcpyDeviceToHost));
-        RPQ_CUDA_TRY(cudaMemcpy(&p_last, cand + j1, 4, cudaMemcpyDeviceToHost));
-    }
+    const uint32_t p_first = p_first_d, p_last = p_last_d;
     HM("p_first/p_last");
     uint64_t R_max = 0;
     for (uint32_t q = 0; q < a->nq; ++q) {
@@ -1989,11 +2002,9 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             bool use = force_sparse;
             if (!use) {
                 const uint64_t ns = std::min<uint64_t>(np, 2048);
-                std::vector<uint32_t> hidx(ns);
-                for (uint64_t k = 0; k < ns; ++k) hidx[k] = (uint32_t)(k * np / ns);
                 uint32_t *didx = (uint32_t *)ws.get(ns * 4);
                 if (!didx) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
-                RPQ_CUDA_TRY(cudaMemcpyAsync(didx, hidx.data(), ns * 4, cudaMemcpyHostToDevice, s));
+                k_sample_idx<<<grid_for(ns), 256, 0, s>>>(didx, ns, np);   // k * np / ns, evenly spread
                 k_sparse<false, false><<<grid_for(ns * 32, SP_WARPS * 32, 148 * 8), SP_WARPS * 32, 0, s>>>(
                     A, cand, pidx, didx, ns, B, 0, 1, sc, sov, d_stats);
                 // overflow flags of the sampled indices, summed on the device
@@ -2323,8 +2334,8 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     Layout *d_layouts = (Layout *)ws.get(std::max<size_t>(lay_h.size(), 1) * sizeof(Layout));
     if (!d_layouts) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
     if (!lay_h.empty()) {
+        // pageable source: the copy is staged before the call returns
         RPQ_CUDA_TRY(cudaMemcpyAsync(d_layouts, lay_h.data(), lay_h.size() * sizeof(Layout), cudaMemcpyHostToDevice, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
     }
     RPQ_CUDA_TRY(cudaMemsetAsync(d_total, 0, 8, s));
         HM("layouts");
