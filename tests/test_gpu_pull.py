@@ -101,3 +101,19 @@ def test_pull_symmetric_default(nv, npairs, seed, monkeypatch):
             assert st["product_edges"] == int(o["pe"].sum()), (rx, B)
         if rx.endswith("+") and nv >= 2048:   # 32-word chunks (>= 2048 sources per batch)
             assert R.rpq_eval_allpairs(G, a, mode=R.RPQ_STATS).stats()["pull_levels"] > 0
+
+
+@pytest.mark.parametrize("pull", ["0", "2"])
+def test_host_driven_level_loop(pull, monkeypatch):
+    """RPQ_HOST_LOOP=1 (the fallback when the conditional CUDA graph cannot be
+    built, and the mode ncu profiles) gives the same pairs and PE."""
+    monkeypatch.setenv("RPQ_HOST_LOOP", "1")
+    monkeypatch.setenv("RPQ_PULL", pull)
+    g = synth.rmat_graph(14, seed=3)          # skewed degrees: rows > HUB_EDGES (742 edges)
+    G = R.rpq_graph_load(g, in_edges=True)
+    for rx in ["(a|b)*c*", "a b* c"]:
+        a = R.rpq_compile(G, rx)
+        o = oracle.allpairs(g, rx)
+        r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_PAIRS | R.RPQ_STATS, batch_sources=2048)
+        assert np.array_equal(r.rows(), sorted_rows(o)), rx
+        assert r.stats()["product_edges"] == int(o["pe"].sum()), rx
