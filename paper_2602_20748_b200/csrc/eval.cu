@@ -904,13 +904,61 @@ __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const 
     }
 }
 
+// Level 0 without q0 rows, short seed rows: a THREAD per batch source ORs
+// its single bit into every neighbour's visited word (and marks the target
+// chunk active); one bit per source means the warp-per-source path below
+// would keep 31 lanes idle (knows+: 65 K sources x ~61 edges took 2.6 ms).
+// Rows with more than SEED_LANE_MAX edges stay with the warp path.  XB is
+// set afterwards from X (k_xb_from_x) instead of one contended OR per edge.
+constexpr uint32_t SEED_LANE_MAX = 256;
+__global__ void __launch_bounds__(256) k_seed_lanes(const DevAuto A, const Layout *__restrict__ Sg,
+                                                    const LevelArgs p, const uint32_t *__restrict__ cand,
+                                                    const uint32_t *__restrict__ pidx, uint64_t b0, uint32_t nb) {
+    __shared__ Layout S;
+    load_layout(S, Sg, A.nq);
+    bool act = false;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+        const uint32_t sv = cand[pidx[b0 + i]];
+        const uint32_t w = i >> 6, c = w / p.cw;
+        const uint64_t bit = 1ull << (i & 63);
+        for (int t = A.toff[0]; t < A.toff[1]; ++t) {
+            const int slot = A.tslot[t];
+            const uint32_t beg = __ldg(A.off[slot] + sv), end = __ldg(A.off[slot] + sv + 1);
+            if (end == beg || end - beg > SEED_LANE_MAX) continue;
+            const uint32_t q2 = A.tto[t];
+            const bool live2 = A.toff[q2 + 1] > A.toff[q2];
+            const uint64_t tbase = S.row_base[q2] - S.lo[q2];
+            for (uint32_t j = beg; j < end; ++j) {
+                const uint64_t trow = tbase + __ldg(A.nbr[slot] + j);
+                red_or64(p.Vis + trow * p.nw + w, bit);
+                if (live2) {
+                    red_or32(p.Xnext + trow * p.nxw + (c >> 5), 1u << (c & 31u));
+                    act = true;
+                }
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, act) && (threadIdx.x & 31) == 0) p.ctrl->active[p.par ^ 1] = 1u;
+}
+
+__global__ void k_xb_from_x(const uint32_t *X, uint64_t nxwords, uint32_t *XB) {
+    for (uint64_t i0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) & ~31ull; i0 < nxwords;
+         i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + (threadIdx.x & 31);
+        const bool nz = i < nxwords && X[i] != 0u;
+        if (__ballot_sync(0xffffffffu, nz) && (threadIdx.x & 31) == 0)
+            atomicOr(XB + (i0 >> 10), 1u << ((i0 >> 5) & 31));
+    }
+}
+
 // Level 0 without q0 rows: a warp per batch source expands its single bit
 // along q0's transitions straight into N / X / XB of the parity-0 level.
 // p must be the parity-1 argument set (its "next" buffers are parity 0).
 template <bool STATS>
 __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layout *__restrict__ Sg,
                                                      const LevelArgs p, const uint32_t *__restrict__ cand,
-                                                     const uint32_t *__restrict__ pidx, uint64_t b0, uint32_t nb) {
+                                                     const uint32_t *__restrict__ pidx, uint64_t b0, uint32_t nb,
+                                                     int long_only) {
     __shared__ Layout S;
     load_layout(S, Sg, A.nq);
     const int lane = threadIdx.x & 31;
@@ -930,6 +978,7 @@ __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layo
             const int slot = A.tslot[t];
             const uint32_t beg = __ldg(A.off[slot] + sv), end = __ldg(A.off[slot] + sv + 1);
             if (STATS && lane == 0) st[S_ITEM_TRANS]++;
+            if (long_only && end - beg <= SEED_LANE_MAX) continue;   // done by k_seed_lanes
             if (end - beg > HUB_EDGES) {
                 // long seed row (e.g. a single target with 10^5 in-edges):
                 // its HUB_EDGES segments go to k_level_hub, launched next
@@ -2436,14 +2485,17 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         ST.kernel_launches++;
         if (skip_q0) {
             const int sg = grid_for((uint64_t)nb * 32, 256, 148 * 8);
+            const int seed_lanes = getenv("RPQ_SEED_WARPS") ? 0 : 1;
+            if (seed_lanes) k_seed_lanes<<<grid_for(nb), 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
             if (stats) {
-                k_seed_expand<true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
+                k_seed_expand<true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb, seed_lanes);
                 if (need_hub) k_level_hub<true><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
             } else {
-                k_seed_expand<false><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
+                k_seed_expand<false><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb, seed_lanes);
                 if (need_hub) k_level_hub<false><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
             }
-            ST.kernel_launches += need_hub ? 2 : 1;
+            if (seed_lanes) k_xb_from_x<<<grid_for(nxwords, 256, 148 * 8), 256, 0, s>>>(X0, nxwords, XB0);
+            ST.kernel_launches += (need_hub ? 2 : 1) + (seed_lanes ? 2 : 0);
         }
         PT.mark("seed");
         rpq_status st = RPQ_OK;
