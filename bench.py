@@ -13,6 +13,18 @@ R12 in DESIGN.md) = sum over reached (vertex, state) pairs of the product
 out-degree on the minimal trim DFA -- identical for the GPU path and the
 oracle (pinned by tests).
 
+Multi-GPU: every query goes through the product's distributed call
+(paper_2602_20748_b200.dist.rpq_eval_allpairs_dist): the ranks agree on one
+batch plan (rpq_plan + all-reduce MIN), each evaluates its batches, and the
+counts are all-reduced -- the gather is inside the timed step.
+
+After the cfg2 headline the same run measures BASELINE's north-star
+configuration once (`north_star` object): the WHOLE RMAT-24 (a|b)*c*
+all-pairs COUNT over all N ranks (configs[4]), asserted against its known
+count, with exact PE from the count pass (RPQ_PE); and the cfg3 LDBC SF10
+queries (`cfg3` object).  Both graphs are generated on a background thread
+while cfg2 runs.  `--no-north-star` / `--no-cfg3` skip them.
+
 `--impl reference` times the CPU oracle (oracle/, O1) on a bounded seeded
 sample of the same workload, on the host cores (rank 0 only).
 """
@@ -45,6 +57,11 @@ WORKLOADS = {
     "cfg5": {"queries": ["(a|b)*c*"],
              "desc": "R-MAT scale 24 (16.8M vertices, 2^28 edge samples), Graph500 A,B,C,D, 8 labels, seed 24"},
 }
+
+
+# |R((a|b)*c*)| on rmat_graph(24, seed=24): the whole all-pairs query, summed
+# over the 16 shards and equal to the 1-GPU run (round 1)
+RMAT24_COUNT = 27_130_980_830_746
 
 
 def make_graph(name):
@@ -139,10 +156,36 @@ def algorithmic_bytes(st):
 
 
 # --------------------------------------------------------------------------
+class GraphMaker:
+    """Generates the north-star / cfg3 graphs on a background thread while the
+    headline runs (numpy releases the GIL in the heavy array ops)."""
+
+    def __init__(self, names):
+        self.out, self.err = {}, {}
+        self.t = threading.Thread(target=self._run, args=(list(names),), daemon=True)
+        self.t.start()
+
+    def _run(self, names):
+        for n in names:
+            t0 = time.perf_counter()
+            try:
+                self.out[n] = (make_graph(n), time.perf_counter() - t0)
+            except Exception as e:              # reported in the JSON line
+                self.err[n] = repr(e)
+
+    def get(self, name):
+        while name not in self.out and name not in self.err and self.t.is_alive():
+            time.sleep(0.05)
+        if name in self.err:
+            raise RuntimeError(self.err[name])
+        return self.out[name]
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_2602_20748_b200 as R
+    from paper_2602_20748_b200 import dist as D
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -161,6 +204,12 @@ def run_ours(args):
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     red_dev = "cpu" if one_gpu_test else "cuda"   # device of the reduced scalars
+    extra = []
+    if args.north_star and args.workload == "cfg2":
+        extra.append("cfg5")
+    if args.cfg3 and args.workload == "cfg2":
+        extra.append("cfg3")
+    maker = GraphMaker(extra) if extra else None
     stream = torch.cuda.current_stream()
     sp = stream.cuda_stream
     wl = WORKLOADS[args.workload]
@@ -168,24 +217,47 @@ def run_ours(args):
     G = R.rpq_graph_load(g, device=local, stream=sp)
     queries = wl["queries"]
 
-    # batch width: one batch per rank for N > 1 (round-robin sharding)
-    # the job's batches are shards 0..world-1 of `sample` x world shards; a
-    # sample > 1 (cfg5 on one GPU) evaluates only that fraction of the batches
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # batch width: N = 1 -> automatic (the library sizes it against HBM);
+    # N > 1 -> the ranks agree on one plan (rpq_plan + all-reduce MIN, the
+    # product's dist path).  --sample-shards S (one GPU standing in for one
+    # rank of N x S shards, a testing aid) evaluates 1/S of the batches.
     sample = max(1, args.sample_shards)
     nshard = world * sample
     bsz = {}
     for rx in queries:
         a = R.rpq_compile(G, rx)
-        st0 = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT, stream=sp, shard_index=0,
-                                  shard_count=max(1, nshard)).stats()
-        P, auto_b = st0["productive_sources"], st0["batch_sources"]
         if args.batch:
             bsz[rx] = args.batch
-        elif world > 1 or sample > 1:
-            per = int(-(-P // nshard) + 63) // 64 * 64
-            bsz[rx] = max(64, min(auto_b, per))
+        elif nshard > 1:
+            pl = R.rpq_plan(G, a, mode=R.RPQ_COUNT, shard_count=nshard, stream=sp)
+            bsz[rx] = D.agree_batch_sources(pl["batch_sources"])
         else:
             bsz[rx] = 0
+
+    def eval_count(Gx, a, B, mode):
+        """One query over the job: the product's dist call (the gather is the
+        count all-reduce); with --sample-shards this rank's shard directly."""
+        if sample > 1:
+            r = R.rpq_eval_allpairs(Gx, a, mode=mode, stream=sp, batch_sources=B, shard_index=rank,
+                                    shard_count=nshard)
+            return r.count, r.stats()
+        d = D.rpq_eval_allpairs_dist(Gx, a, mode=mode, stream=sp, batch_sources=B)
+        return d.count, d.local.stats()
+
     # per-rank probe with the in-kernel counters (RPQ_STATS): PE and the
     # algorithmic bytes of this rank's shard
     probe = {}
@@ -198,13 +270,11 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")   # > 126 MB L2
 
     def step(mode):
-        tot = {"count": 0, "pe": 0, "launches": 0, "expand_ms": 0.0, "levels": 0}
+        tot = {"count": 0, "launches": 0, "expand_ms": 0.0, "levels": 0}
         for rx in queries:
             a = R.rpq_compile(G, rx)
-            r = R.rpq_eval_allpairs(G, a, mode=mode, stream=sp, batch_sources=bsz[rx],
-                                    shard_index=rank, shard_count=nshard)
-            st = r.stats()
-            tot["count"] += r.count
+            c, st = eval_count(G, a, bsz[rx], mode)
+            tot["count"] += c
             tot["launches"] += st["kernel_launches"]
             tot["expand_ms"] += st["expand_ms"]
             tot["levels"] += st["levels"]
@@ -244,17 +314,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     if os.environ.get("BENCH_DEBUG"):
         print("step ms:", " ".join(f"{t:.1f}" for t in times), file=sys.stderr)
-    total_ms = float(sum(times))
-    pe_total = probe_pe * args.steps          # PE is a property of (graph, query, shard)
-    if world > 1:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-        pt = torch.tensor([float(pe_total), float(agg["count"])], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(pt, op=dist.ReduceOp.SUM)
-        pe_total, count_total = int(pt[0].item()), int(pt[1].item())
-    else:
-        count_total = agg["count"]
+    total_ms = allmax(float(sum(times)))
+    pe_total = allsum(probe_pe * args.steps)          # PE is a property of (graph, query, shard)
+    # the dist call already summed the count over ranks (sample > 1: this shard only)
+    count_total = agg["count"] if sample == 1 else allsum(agg["count"])
 
     # end to end through the public API: host (pinned) edge arrays -> load ->
     # compile -> evaluate -> counts on the host, every step
@@ -270,22 +333,20 @@ def run_ours(args):
         t0 = time.perf_counter()
         G2 = R.rpq_graph_load(num_vertices=g.num_vertices, src=h_src, dst=h_dst, label=h_lab,
                               label_names=g.label_names, device=local, stream=sp)
-        pe_e = 0
         for rx in queries:
             a = R.rpq_compile(G2, rx)
-            r = R.rpq_eval_allpairs(G2, a, mode=R.RPQ_COUNT, stream=sp, batch_sources=bsz[rx],
-                                    shard_index=rank, shard_count=nshard)
-            _ = r.count                                  # device -> host result
+            _ = eval_count(G2, a, bsz[rx], R.RPQ_COUNT)[0]      # device -> host result
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) * 1e3
         del G2
         if i > 0:
             e2e_ms.append(dt)
-    e2e_step = statistics.median(e2e_ms)
-    if world > 1:
-        tt = torch.tensor([e2e_step], dtype=torch.float64, device=red_dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_step = float(tt.item())
+    e2e_step = allmax(statistics.median(e2e_ms))
+
+    ns = north_star_leg(args, R, D, maker, sp, stream, local, rank, world, allmax, allsum) \
+        if maker and "cfg5" in extra else None
+    c3 = cfg3_leg(args, R, D, maker, sp, stream, local, rank, world, allmax, allsum) \
+        if maker and "cfg3" in extra else None
 
     if rank != 0:
         if world > 1:
@@ -314,7 +375,8 @@ def run_ours(args):
         "config": {"workload": args.workload, "graph": wl["desc"], "queries": queries, "mode": "COUNT",
                    "pe_per_step": pe_per_step, "pairs_per_step": count_total / args.steps,
                    "batch_sources": {rx: probe[rx]["batch_sources"] if not bsz[rx] else bsz[rx] for rx in queries},
-                   "parallelism": f"source-batch shards x{world}",
+                   "parallelism": f"source-batch shards x{world} (rpq_eval_allpairs_dist: agreed batch plan, "
+                                  f"count all-reduce inside the step)",
                    "l2": "flushed between timed steps (256 MiB write)",
                    "sample": "all batches" if sample == 1 else
                              f"batches of shards 0..{world - 1} of {nshard} (1/{sample} of the all-pairs query)"},
@@ -339,7 +401,11 @@ def run_ours(args):
         "gpu_launches": agg["launches"],
         "clocks": clk.summary(),
     }
-    if world == 1 and args.workload != "cfg5":
+    if ns is not None:
+        line["north_star"] = ns
+    if c3 is not None:
+        line["cfg3"] = c3
+    if world == 1 and args.workload != "cfg5" and not args.no_pairs:
         # PAIRS mode (timed separately from the COUNT headline):
         # sorted distinct pairs materialised in device memory, per query
         pr = {}
@@ -363,6 +429,109 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def north_star_leg(args, R, D, maker, sp, stream, local, rank, world, allmax, allsum):
+    """BASELINE north_star / configs[4]: the whole RMAT-24 (a|b)*c* all-pairs
+    COUNT across the N ranks, once, after a warm-up on 1/64 of the batches.
+    PE is exact (RPQ_PE: popcount x product out-degree inside the count
+    pass); the count is asserted against RMAT24_COUNT.  Algorithmic bytes =
+    (bytes per PE of an RPQ_STATS probe on the warm-up sample) x PE."""
+    import torch
+    import torch.distributed as dist
+    g5, gen_s = maker.get("cfg5")
+    t0 = time.perf_counter()
+    G5 = R.rpq_graph_load(g5, device=local, stream=sp)
+    torch.cuda.synchronize()
+    load_s = time.perf_counter() - t0
+    rx = WORKLOADS["cfg5"]["queries"][0]
+    a5 = R.rpq_compile(G5, rx)
+    pl = R.rpq_plan(G5, a5, mode=R.RPQ_COUNT, shard_count=world, stream=sp)
+    B5 = D.agree_batch_sources(pl["batch_sources"])
+    nb = -(-pl["productive_sources"] // B5)
+    # warm-up + algorithmic-bytes probe: this rank's share of 1/64 of the batches
+    R.rpq_eval_allpairs(G5, a5, mode=R.RPQ_COUNT, stream=sp, batch_sources=B5, shard_index=rank,
+                        shard_count=world * 64)
+    pst = R.rpq_eval_allpairs(G5, a5, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=sp, batch_sources=B5,
+                              shard_index=rank, shard_count=world * 64).stats()
+    bytes_per_pe = allsum(algorithmic_bytes(pst)) / max(1.0, allsum(pst["product_edges"]))
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        d = D.rpq_eval_allpairs_dist(G5, a5, mode=R.RPQ_COUNT | R.RPQ_PE | R.RPQ_TIME_KERNELS, stream=sp,
+                                     batch_sources=B5)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = allmax(ev0.elapsed_time(ev1))
+    loop_ms = allmax(d.local.stats()["expand_ms"])
+    pe = int(d.stats["product_edges"])
+    del G5
+    peak, peak_src = load_peaks()
+    traffic = load_traffic("cfg5")
+    alg_bytes = bytes_per_pe * pe
+    # per GPU: its share of the bytes over the whole-query time (the slowest rank)
+    achieved = alg_bytes / world / (ms / 1e3) / 1e9
+    out = {"workload": "cfg5", "graph": WORKLOADS["cfg5"]["desc"], "query": rx, "mode": "COUNT, all-pairs, all batches",
+           "n_gpus": world, "count": d.count, "count_expected": RMAT24_COUNT, "count_ok": d.count == RMAT24_COUNT,
+           "ms": ms, "pe": pe, "pe_per_s": pe / (ms / 1e3), "batches": nb, "batch_sources": B5,
+           "level_loop_ms_max_rank": loop_ms, "graph_gen_s": gen_s, "graph_load_s": load_s,
+           "roofline": {"bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+                        "algorithmic_bytes": alg_bytes, "bytes_per_pe": bytes_per_pe,
+                        "achieved_per_gpu": achieved, "frac": achieved / peak,
+                        "note": "algorithmic bytes per PE from an RPQ_STATS probe of 1/64 of the batches x exact PE; "
+                                "time = whole query (count pass, clears, per-batch setup included), slowest rank",
+                        "ncu_dram_over_algorithmic": (traffic["dram_bytes_per_launch"] /
+                                                      traffic["algorithmic_bytes_per_launch"])
+                        if traffic and traffic.get("algorithmic_bytes_per_launch") else None},
+           "clocks": clk.summary()}
+    if not out["count_ok"] and rank == 0:
+        print(f"north_star: count {d.count} != expected {RMAT24_COUNT}", file=sys.stderr)
+    return out
+
+
+def cfg3_leg(args, R, D, maker, sp, stream, local, rank, world, allmax, allsum):
+    """BASELINE configs[2]: LDBC-SNB-shaped SF10 graph, replyOf* and knows+
+    all-pairs COUNT over the N ranks (source-sharded); median of 3 after 3
+    warm-ups, exact PE from the count pass (RPQ_PE)."""
+    import torch
+    import torch.distributed as dist
+    g3, gen_s = maker.get("cfg3")
+    G3 = R.rpq_graph_load(g3, device=local, stream=sp)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    res = {}
+    tot_ms, tot_pe = 0.0, 0
+    for rx in WORKLOADS["cfg3"]["queries"]:
+        a = R.rpq_compile(G3, rx)
+        B = 0
+        if world > 1:
+            B = D.agree_batch_sources(R.rpq_plan(G3, a, shard_count=world, stream=sp)["batch_sources"])
+        m = R.RPQ_COUNT | R.RPQ_PE
+        for _ in range(3):
+            d = D.rpq_eval_allpairs_dist(G3, a, mode=m, stream=sp, batch_sources=B)
+        ts = []
+        for _ in range(3):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            d = D.rpq_eval_allpairs_dist(G3, a, mode=m, stream=sp, batch_sources=B)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(allmax(ev0.elapsed_time(ev1)))
+        ms = statistics.median(ts)
+        pe = int(d.stats["product_edges"])
+        res[rx] = {"count": d.count, "pe": pe, "ms": ms, "pe_per_s": pe / (ms / 1e3),
+                   "batch_sources": d.batch_sources}
+        tot_ms += ms
+        tot_pe += pe
+    del G3
+    return {"workload": "cfg3", "graph": WORKLOADS["cfg3"]["desc"], "n_gpus": world, "queries": res,
+            "ms": tot_ms, "pe": tot_pe, "pe_per_s": tot_pe / (tot_ms / 1e3), "graph_gen_s": gen_s}
 
 
 # --------------------------------------------------------------------------
@@ -450,6 +619,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-north-star", dest="north_star", action="store_false",
+                    help="skip the whole-RMAT-24 (a|b)*c* north-star measurement")
+    ap.add_argument("--no-cfg3", dest="cfg3", action="store_false", help="skip the LDBC SF10 cfg3 measurement")
+    ap.add_argument("--no-pairs", action="store_true", help="skip the PAIRS-mode measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

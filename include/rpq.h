@@ -144,6 +144,10 @@ rpq_status rpq_nfa_reverse(const rpq_nfa *a, rpq_nfa **out);
 #define RPQ_PER_SOURCE 4u     /* per-source result counts */
 #define RPQ_STATS 8u          /* count PE / word ops / items (small overhead) */
 #define RPQ_TIME_KERNELS 16u  /* CUDA-event time of every expand launch */
+#define RPQ_PE 32u            /* product_edges (PE, reading R12) from the post-pass only (no in-kernel
+                                 counters); in COUNT mode fused into the count pass */
+#define RPQ_SOURCE_PE 64u     /* with RPQ_PER_SOURCE: per-source PE (rpq_result_source_pe); the
+                                 per-source list then holds every source with a non-zero count OR PE */
 
 typedef struct {
     uint32_t mode;              /* OR of the RPQ_* mode bits above; 0 = RPQ_COUNT */
@@ -158,9 +162,29 @@ typedef struct {
 
 /* All-pairs: x ranges over all of V (R11).  With shard_count > 1 the result
  * holds only this shard's batches (sources are cut into batches of B
- * consecutive productive sources; batch b belongs to shard b % count). */
+ * consecutive productive sources; batch b belongs to shard b % count).
+ * Every rank must derive the same batches, so shard_count > 1 requires
+ * batch_sources or hbm_budget_bytes (EINVAL otherwise); with an explicit
+ * budget the automatic B is also capped at ceil(|P| / shard_count) rounded
+ * up to 64 so that every shard gets work. */
 rpq_status rpq_eval_allpairs(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
                              rpq_result **out);
+/* The batch plan rpq_eval_allpairs would use with these options, without
+ * evaluating anything (device work: the productive-source scan of
+ * Challenge 2's batching): |P|, the batch width B (auto unless
+ * opts->batch_sources is set), the number of batches, the 64-bit words per
+ * state array and the chunk width.  Ranks of a sharded evaluation call it,
+ * agree on the minimum B (all-reduce MIN) and pass it as batch_sources.
+ * Errors as rpq_eval_allpairs; EINVAL for NULL arguments. */
+typedef struct {
+    uint64_t productive_sources;
+    uint32_t batch_sources;
+    uint32_t chunk_words;
+    uint64_t num_batches;
+    uint64_t state_words;
+} rpq_plan_info;
+rpq_status rpq_plan(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts, rpq_plan_info *info);
+
 /* Single source x = src.  src >= |V| -> EINVAL. */
 rpq_status rpq_eval_single_source(const rpq_graph *g, const rpq_nfa *a, uint32_t src,
                                   const rpq_eval_opts *opts, rpq_result **out);
@@ -191,7 +215,8 @@ rpq_status rpq_eval_single_target(const rpq_graph *g, const rpq_nfa *a, uint32_t
  * source always forms a chunk), each chunk in PAIRS mode, and its pairs are
  * copied through two pinned host buffers so that the copy of piece k+1
  * overlaps the sink of piece k.  Sharding: chunk c belongs to shard
- * c % shard_count.  *total = pairs delivered.  A sink returning non-zero
+ * c % shard_count; the chunks follow device_budget_bytes, so a sharded call
+ * must pass the same non-zero budget on every rank (EINVAL if 0).  *total = pairs delivered.  A sink returning non-zero
  * stops the evaluation early (RPQ_OK; *total counts what was delivered).
  * Errors as rpq_eval_allpairs; EINVAL for a NULL sink. */
 typedef int (*rpq_pairs_sink)(const uint32_t *src, const uint32_t *dst, uint64_t n, void *ctx);
@@ -266,7 +291,27 @@ rpq_status rpq_result_copy_host(const rpq_result *r, uint32_t *const *cols, uint
  * non-zero count, ascending source; host buffers, ECAPACITY as above */
 rpq_status rpq_result_source_counts(const rpq_result *r, uint32_t *srcs, uint64_t *counts,
                                     uint64_t cap, uint64_t *n);
+/* RPQ_PER_SOURCE | RPQ_SOURCE_PE: product edges traversed per listed source
+ * (same order as rpq_result_source_counts): sum over the (vertex, state)
+ * pairs the source reaches of the product out-degree on the minimal trim DFA
+ * (reading R12).  Host buffer; ECAPACITY as above; EINVAL if
+ * the result has no per-source PE. */
+rpq_status rpq_result_source_pe(const rpq_result *r, uint64_t *pe, uint64_t cap, uint64_t *n);
 rpq_status rpq_result_stats(const rpq_result *r, rpq_stats *s);
+/* PAIRS results of rpq_eval_allpairs / rpq_eval_sources (and PER_SOURCE
+ * results of the dense engine; other results: no entries): the batches this
+ * shard evaluated, in order.  Batch k covers the candidate
+ * sources [cand_lo, cand_hi) (indices into the sorted candidate list; the
+ * vertex ids themselves for all-pairs) and owns result rows [offset,
+ * offset + count); batches of all shards, sorted by cand_lo, tile the
+ * global (src, dst)-sorted result -- which is how a multi-GPU gather places
+ * every shard's rows.  Host buffer of capacity
+ * cap entries; *n = entries (ECAPACITY if cap < *n; 0 for other modes). */
+typedef struct {
+    uint64_t cand_lo, cand_hi;
+    uint64_t offset, count;
+} rpq_batch_info;
+rpq_status rpq_result_batches(const rpq_result *r, rpq_batch_info *out, uint64_t cap, uint64_t *n);
 void rpq_result_free(rpq_result *r);
 
 /* Host-only: the shard that owns each candidate source under the batch plan
@@ -295,8 +340,11 @@ rpq_status rpq_trim_memory(int device);
  * caching allocator): alloc(bytes, stream, ctx) returns device memory usable
  * in stream order on `stream` (NULL on failure -> RPQ_ENOMEM), free_(ptr,
  * stream, ctx) releases it.  Both NULL restores the pool.  Set it before any
- * graph/evaluation whose buffers it would free (results free their buffers
- * through the allocator current at rpq_result_free).  Process-wide.
+ * graph/evaluation whose buffers it should hold: graphs and results free
+ * their buffers through the allocator that was installed when they were
+ * created (so the functions must stay valid until then), results on the
+ * stream of the evaluation that made them (that stream must outlive the
+ * result).  Process-wide.
  * EINVAL if exactly one of the two functions is NULL. */
 rpq_status rpq_set_allocator(void *(*alloc)(size_t bytes, void *stream, void *ctx),
                              void (*free_)(void *ptr, void *stream, void *ctx), void *ctx);

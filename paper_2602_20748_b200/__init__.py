@@ -32,6 +32,7 @@ RPQ_ENOMEM, RPQ_ECUDA, RPQ_ECAPACITY, RPQ_EUNSUPPORTED = -4, -5, -6, -7
 RPQ_SYNTAX_PAPER, RPQ_NO_MINIMIZE = 1, 2
 RPQ_MAX_STATES, RPQ_MAX_TRANSITIONS, RPQ_MAX_QUERY_LABELS = 64, 256, 32
 RPQ_COUNT, RPQ_PAIRS, RPQ_PER_SOURCE, RPQ_STATS, RPQ_TIME_KERNELS = 1, 2, 4, 8, 16
+RPQ_PE, RPQ_SOURCE_PE = 32, 64
 RPQ_GRAPH_IN_EDGES = 1
 RPQ_MAX_COLS = 16
 
@@ -65,6 +66,17 @@ class rpq_eval_opts(ctypes.Structure):
                 ("hbm_budget_bytes", ctypes.c_uint64), ("shard_index", ctypes.c_uint32),
                 ("shard_count", ctypes.c_uint32), ("cuda_stream", ctypes.c_void_p),
                 ("chunk_words", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
+class rpq_plan_info(ctypes.Structure):
+    _fields_ = [("productive_sources", ctypes.c_uint64), ("batch_sources", ctypes.c_uint32),
+                ("chunk_words", ctypes.c_uint32), ("num_batches", ctypes.c_uint64),
+                ("state_words", ctypes.c_uint64)]
+
+
+class rpq_batch_info(ctypes.Structure):
+    _fields_ = [("cand_lo", ctypes.c_uint64), ("cand_hi", ctypes.c_uint64),
+                ("offset", ctypes.c_uint64), ("count", ctypes.c_uint64)]
 
 
 class crpq_query(ctypes.Structure):
@@ -113,7 +125,7 @@ EXPORTED = [
     "rpq_result_source_counts", "rpq_result_stats", "rpq_result_free", "rpq_last_error",
     "rpq_device_count", "rpq_version", "rpq_shard_plan", "rpq_trim_memory",
     "rpq_nfa_reverse", "rpq_eval_targets", "rpq_eval_single_target", "rpq_eval_allpairs_stream",
-    "rpq_set_allocator",
+    "rpq_set_allocator", "rpq_plan", "rpq_result_batches", "rpq_result_source_pe",
 ]
 
 _c = {}
@@ -154,6 +166,9 @@ _c["rpq_result_source_counts"] = _proto("rpq_result_source_counts", _st, [_vp, c
                                                                           c_u64p])
 _c["rpq_result_stats"] = _proto("rpq_result_stats", _st, [_vp, _P(rpq_stats)])
 _c["rpq_result_free"] = _proto("rpq_result_free", None, [_vp])
+_c["rpq_result_batches"] = _proto("rpq_result_batches", _st, [_vp, _P(rpq_batch_info), ctypes.c_uint64, c_u64p])
+_c["rpq_plan"] = _proto("rpq_plan", _st, [_vp, _vp, _P(rpq_eval_opts), _P(rpq_plan_info)])
+_c["rpq_result_source_pe"] = _proto("rpq_result_source_pe", _st, [_vp, c_u64p, ctypes.c_uint64, c_u64p])
 _c["rpq_last_error"] = _proto("rpq_last_error", ctypes.c_char_p, [])
 _c["rpq_device_count"] = _proto("rpq_device_count", _st, [_P(ctypes.c_int)])
 _c["rpq_version"] = _proto("rpq_version", ctypes.c_char_p, [])
@@ -276,6 +291,29 @@ class Result:
                                               ctypes.byref(n)))
         return s[:k], c[:k]
 
+    def source_pe(self) -> np.ndarray:
+        """Per-source PE (RPQ_PER_SOURCE | RPQ_SOURCE_PE), aligned with source_counts()."""
+        n = ctypes.c_uint64()
+        st = _c["rpq_result_source_pe"](self.h, None, 0, ctypes.byref(n))
+        if st not in (RPQ_OK, RPQ_ECAPACITY):
+            _check(st)
+        k = n.value
+        pe = np.zeros(max(k, 1), np.uint64)
+        _check(_c["rpq_result_source_pe"](self.h, _ptr(pe, ctypes.c_uint64), k, ctypes.byref(n)))
+        return pe[:k]
+
+    def batches(self) -> np.ndarray:
+        """(k, 4) uint64 rows (cand_lo, cand_hi, offset, count) of this
+        shard's batches (PAIRS results; see rpq_result_batches)."""
+        n = ctypes.c_uint64()
+        st = _c["rpq_result_batches"](self.h, None, 0, ctypes.byref(n))
+        if st not in (RPQ_OK, RPQ_ECAPACITY):
+            _check(st)
+        k = n.value
+        buf = (rpq_batch_info * max(k, 1))()
+        _check(_c["rpq_result_batches"](self.h, buf, k, ctypes.byref(n)))
+        return np.array([[b.cand_lo, b.cand_hi, b.offset, b.count] for b in buf[:k]], np.uint64).reshape(k, 4)
+
     def __del__(self):
         if getattr(self, "h", None) and _c:
             _c["rpq_result_free"](self.h)
@@ -293,7 +331,10 @@ def rpq_version() -> str:
     return _c["rpq_version"]().decode()
 
 
-_allocator_refs = None
+# every allocator ever installed stays referenced: graphs and results free
+# their buffers through the allocator that allocated them, which may have
+# been replaced (or removed) since
+_allocator_refs = []
 
 
 def rpq_set_allocator(alloc=None, free=None) -> None:
@@ -301,14 +342,12 @@ def rpq_set_allocator(alloc=None, free=None) -> None:
     both None restores the library's stream-ordered pool.  Example (PyTorch's
     caching allocator): alloc=lambda n, s: torch.cuda.caching_allocator_alloc(n, stream=s),
     free=lambda p, s: torch.cuda.caching_allocator_delete(p)."""
-    global _allocator_refs
     if alloc is None and free is None:
         _check(_c["rpq_set_allocator"](RPQ_ALLOC_FN(), RPQ_FREE_FN(), None))
-        _allocator_refs = None
         return
     fa = RPQ_ALLOC_FN(lambda n, s, _ctx: alloc(int(n), s or 0) or None)
     ff = RPQ_FREE_FN(lambda p, s, _ctx: free(p, s or 0))
-    _allocator_refs = (fa, ff)      # keep the thunks alive while installed
+    _allocator_refs.append((fa, ff))      # keep the thunks alive for good
     _check(_c["rpq_set_allocator"](fa, ff, None))
 
 
@@ -417,6 +456,22 @@ def rpq_eval_allpairs(g: Graph, a: Nfa, opts: Optional[rpq_eval_opts] = None, **
     h = ctypes.c_void_p()
     _check(_c["rpq_eval_allpairs"](g.h, a.h, ctypes.byref(o), ctypes.byref(h)))
     return Result(h.value)
+
+
+def rpq_plan(g: Graph, a: Nfa, opts: Optional[rpq_eval_opts] = None, **kw) -> dict:
+    """Batch plan of rpq_eval_allpairs under these options (nothing evaluated)."""
+    o = opts if opts is not None else make_opts(**kw)
+    info = rpq_plan_info()
+    _check(_c["rpq_plan"](g.h, a.h, ctypes.byref(o), ctypes.byref(info)))
+    return {k: getattr(info, k) for k, _ in info._fields_}
+
+
+def rpq_result_batches(r: Result) -> np.ndarray:
+    return r.batches()
+
+
+def rpq_result_source_pe(r: Result) -> np.ndarray:
+    return r.source_pe()
 
 
 def rpq_eval_single_source(g: Graph, a: Nfa, src: int, opts: Optional[rpq_eval_opts] = None, **kw) -> Result:

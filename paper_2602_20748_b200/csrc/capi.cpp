@@ -160,6 +160,24 @@ void dev_free(void *p, void *stream) {
     else cudaFreeAsync(p, (cudaStream_t)stream);
 }
 
+AllocSnap *alloc_snapshot() {
+    const UserAlloc ua = user_alloc();
+    AllocSnap *s = new AllocSnap();
+    s->alloc = ua.alloc;
+    s->free_ = ua.free_;
+    s->ctx = ua.ctx;
+    return s;
+}
+
+// free with the allocator captured when the block was allocated (not the
+// one installed now); no snapshot = the current one
+void dev_free_snap(void *p, void *stream, const AllocSnap *snap) {
+    if (!p) return;
+    if (!snap) { dev_free(p, stream); return; }
+    if (snap->free_) snap->free_(p, stream, snap->ctx);
+    else cudaFreeAsync(p, (cudaStream_t)stream);
+}
+
 // ---- automaton -----------------------------------------------------------
 extern "C" rpq_status rpq_compile(const rpq_graph *vocab, const char *regex, uint32_t flags,
                                   rpq_nfa **out, size_t *err_offset) {
@@ -231,12 +249,15 @@ void rpq_result_release(rpq_result *r) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(r->device);
-    // result buffers come from the stream-ordered pool (dev_alloc): freed
-    // back to it, ordered on the legacy default stream
-    for (uint32_t c = 0; c < RPQ_MAX_COLS; ++c) if (r->cols[c]) dev_free(r->cols[c], nullptr);
-    if (r->ps_src) dev_free(r->ps_src, nullptr);
-    if (r->ps_cnt) dev_free(r->ps_cnt, nullptr);
+    // result buffers come from dev_alloc on the evaluation's stream: freed
+    // on that stream (ordered after the caller's work queued there) through
+    // the allocator that allocated them
+    for (uint32_t c = 0; c < RPQ_MAX_COLS; ++c) if (r->cols[c]) dev_free_snap(r->cols[c], r->stream, r->alloc_snap);
+    if (r->ps_src) dev_free_snap(r->ps_src, r->stream, r->alloc_snap);
+    if (r->ps_cnt) dev_free_snap(r->ps_cnt, r->stream, r->alloc_snap);
+    if (r->ps_pe) dev_free_snap(r->ps_pe, r->stream, r->alloc_snap);
     cudaSetDevice(prev);
+    delete r->alloc_snap;
     delete r;
 }
 
@@ -275,6 +296,25 @@ extern "C" rpq_status rpq_result_source_counts(const rpq_result *r, uint32_t *sr
         if (srcs) RPQ_CUDA_TRY(cudaMemcpy(srcs, r->ps_src, r->n_ps * 4, cudaMemcpyDeviceToHost));
         if (counts) RPQ_CUDA_TRY(cudaMemcpy(counts, r->ps_cnt, r->n_ps * 8, cudaMemcpyDeviceToHost));
     }
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_result_batches(const rpq_result *r, rpq_batch_info *out, uint64_t cap, uint64_t *n) {
+    if (!r) return rpq_fail(RPQ_EINVAL, "NULL result");
+    if (n) *n = r->batches.size();
+    if (cap < r->batches.size()) return rpq_fail(RPQ_ECAPACITY, "need %zu", r->batches.size());
+    if (!out && !r->batches.empty()) return rpq_fail(RPQ_EINVAL, "NULL output");
+    for (size_t i = 0; i < r->batches.size(); ++i) out[i] = r->batches[i];
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_result_source_pe(const rpq_result *r, uint64_t *pe, uint64_t cap, uint64_t *n) {
+    if (!r) return rpq_fail(RPQ_EINVAL, "NULL result");
+    if (n) *n = r->ps_pe ? r->n_ps : 0;
+    if (!r->ps_pe) return rpq_fail(RPQ_EINVAL, "result was not evaluated with RPQ_PER_SOURCE | RPQ_SOURCE_PE");
+    if (cap < r->n_ps) return rpq_fail(RPQ_ECAPACITY, "need %llu", (unsigned long long)r->n_ps);
+    cudaSetDevice(r->device);
+    if (r->n_ps && pe) RPQ_CUDA_TRY(cudaMemcpy(pe, r->ps_pe, r->n_ps * 8, cudaMemcpyDeviceToHost));
     return RPQ_OK;
 }
 

@@ -453,6 +453,8 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
 
     // ---- lexicographic order in variable order: stable LSD radix passes ----
     rpq_result *res = new rpq_result();
+    res->stream = (void *)s;
+    res->alloc_snap = alloc_snapshot();
     res->device = g->device;
     res->ncols = nvars;
     res->nrows = T.n;

@@ -118,12 +118,6 @@ struct Ctrl {                  // per-level device counters / flags
     uint32_t ntouched;         // entries of LevelArgs::TL
     uint32_t pcur[2];          // pull-level task cursor per parity
     uint32_t hcur;             // hub-record cursor (reset per level and before the seed hub launch)
-    // adaptive direction: a pull level counts the chunk-words that needed bits
-    // and those it completed; if fewer than half complete (directed graphs
-    // where most sources never reach most vertices), the batch stays top-down
-    unsigned long long pull_need, pull_done;
-    uint32_t pull_off;
-    uint32_t pad;
 };
 
 // One BFS level over the rows whose activity bit is set in (Xcur, XBcur).
@@ -178,7 +172,7 @@ __device__ __forceinline__ void red_or32(uint32_t *p, uint32_t v) {
 // Bottom-up when enabled for the query (symmetric relations, or forced) and
 // at least 10 % of the work units are active (a dense frontier).
 __device__ __forceinline__ bool level_pull(const LevelArgs &p) {
-    if (!p.pull_mode || *(volatile const uint32_t *)&p.ctrl->pull_off) return false;
+    if (!p.pull_mode) return false;
     const uint32_t n = *(volatile const uint32_t *)&p.ctrl->ucnt[p.par];
     return n != 0 && (uint64_t)n * 10ull > p.total_units;
 }
@@ -227,7 +221,6 @@ __global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
         p.ctrl->ucur[par ^ 1] = 0;
         p.ctrl->pcur[par] = 0;
         p.ctrl->active[par ^ 1] = 0;   // set by this level's activations
-        p.ctrl->pull_need = p.ctrl->pull_done = 0;
 
         p.ctrl->nhub_items = 0;
         p.ctrl->nhub_recs = 0;
@@ -323,14 +316,23 @@ __global__ void k_clear_touched(const LevelArgs p, uint64_t nunits, int force_de
 // COUNT over the touched chunks only: bits of Vis[q][v][w] for final q that
 // are not already set in a lower-numbered final state's row of v (the OR over
 // final states, counted once).
+// pe != nullptr: also the product edges of the touched chunks (popcount x
+// product out-degree of (v, q), reading R12) -- every reached bit of a row
+// with outgoing transitions lies in a touched chunk.
+__device__ __forceinline__ uint32_t prod_deg(const DevAuto &A, int q, uint32_t v) {
+    uint32_t d = 0;
+    for (int t = A.toff[q]; t < A.toff[q + 1]; ++t) d += __ldg(A.off[A.tslot[t]] + v + 1) - __ldg(A.off[A.tslot[t]] + v);
+    return d;
+}
+
 __global__ void k_count_touched(const DevAuto A, const Layout S, const LevelArgs p, uint64_t nunits,
-                                unsigned long long *total, int force_dense) {
+                                unsigned long long *total, int force_dense, unsigned long long *pe = nullptr) {
     const uint32_t ntl = p.ctrl->ntouched;
     if (force_dense || (uint64_t)ntl * 4 > nunits) return;      // dense batch: k_count_total counts
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    unsigned long long acc = 0;
+    unsigned long long acc = 0, pacc = 0;
     for (uint64_t t = wid; t < ntl; t += nwarps) {
         const uint64_t u = p.TL[t];
         const uint64_t xi_l = u * 32 + lane;
@@ -344,14 +346,18 @@ __global__ void k_count_touched(const DevAuto A, const Layout S, const LevelArgs
             const uint64_t row = xi / p.nxw;
             const uint32_t xw = (uint32_t)(xi % p.nxw);
             const int q = row_state(S, A.nq, row);
-            if (!((A.final_mask >> q) & 1ull)) continue;
+            const bool fin = (A.final_mask >> q) & 1ull;
             const uint32_t v = S.lo[q] + (uint32_t)(row - S.row_base[q]);
+            const uint32_t deg = pe ? prod_deg(A, q, v) : 0u;
+            if (!fin && !deg) continue;
             while (x) {
                 const uint32_t bt = (uint32_t)(__ffs(x) - 1);
                 x &= x - 1;
                 const uint64_t col = (uint64_t)(xw * 32u + bt) * p.cw + lane;
                 if (lane >= (int)p.cw || col >= p.nw) continue;
                 uint64_t w = ld_cg(p.Vis + row * p.nw + col);
+                pacc += (unsigned long long)__popcll(w) * deg;
+                if (!fin) continue;
                 for (int f = 0; f < q && w; ++f)
                     if (((A.final_mask >> f) & 1ull) && v - S.lo[f] < S.len[f])
                         w &= ~ld_cg(p.Vis + (S.row_base[f] + (v - S.lo[f])) * p.nw + col);
@@ -360,8 +366,12 @@ __global__ void k_count_touched(const DevAuto A, const Layout S, const LevelArgs
         }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = 16; o; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        pacc += __shfl_xor_sync(0xffffffffu, pacc, o);
+    }
     if (lane == 0 && acc) atomicAdd(total, acc);
+    if (lane == 0 && pacc) atomicAdd(pe, pacc);
 }
 
 __global__ void k_level_end(Ctrl *ctrl, cudaGraphConditionalHandle h) {
@@ -777,7 +787,6 @@ __global__ void __launch_bounds__(256) k_pull(const DevAuto A, const Layout *__r
     const uint32_t nch = p.nw / 32u;
     const uint64_t ntask = nrows * nch;
     unsigned long long st[NSTAT] = {};
-    unsigned long long cnt_need = 0, cnt_done = 0;
     bool act = false;
     for (;;) {
         uint32_t t0 = 0;
@@ -800,11 +809,6 @@ __global__ void __launch_bounds__(256) k_pull(const DevAuto A, const Layout *__r
             const uint32_t v = S.lo[q2] + (uint32_t)(row - S.row_base[q2]);
             const uint64_t acc = pull_gather<STATS>(A, S, p, q2, v, col, need, lane, st);
             const uint64_t nb = need & acc;
-            {   // words that needed bits / that this level completed
-                const unsigned nm = __ballot_sync(0xffffffffu, need != 0);
-                const unsigned fm = __ballot_sync(0xffffffffu, need != 0 && nb == need);
-                if (lane == 0) { cnt_need += __popc(nm); cnt_done += __popc(fm); }
-            }
             if (nb) {
                 p.Vis[wi] = vis | nb;                      // single owner of the word in a pull level
                 act_or(actS, p.ActNext, col, nb);
@@ -818,10 +822,6 @@ __global__ void __launch_bounds__(256) k_pull(const DevAuto A, const Layout *__r
         }
     }
     if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
-    if (lane == 0 && cnt_need) {
-        atomicAdd(&p.ctrl->pull_need, cnt_need);
-        atomicAdd(&p.ctrl->pull_done, cnt_done);
-    }
     if (STATS && threadIdx.x == 0 && blockIdx.x == 0) st[S_PULL_LEVELS] = 1;
     flush_stats<STATS>(st, p.stats);
     act_flush(actS, p.ActNext, p.nw);
@@ -852,6 +852,61 @@ __global__ void k_pe_rows(const DevAuto A, const Layout S, const uint64_t *Vis, 
         acc += pc * deg;
     }
     if (lane == 0 && acc) atomicAdd(out, acc);
+}
+
+// Per-source PE (RPQ_SOURCE_PE): pe[i] += sum over rows (q, v) with bit i in
+// Vis of the product out-degree of (v, q).  A warp takes a tile of 32 rows x 4
+// words: lane = row, and for every bit position the warp sums the out-degrees
+// of the rows that have it with one REDUX (__reduce_add_sync); lane b keeps
+// bits b and b + 32.  A verification mode (parity of the PE numerator per
+// source), not on the timed path.
+constexpr uint32_t SPE_TILES = 64;   // 32-row tiles per task (atomics amortised)
+__global__ void k_source_pe(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t nw, uint32_t nb,
+                            unsigned long long *pe) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    const uint64_t nrows = S.row_base[A.nq - 1] + S.len[A.nq - 1];
+    const uint64_t ntiles = (nrows + 31) / 32, ngrp = (nw + 3) / 4;
+    const uint64_t nchunks = (ntiles + SPE_TILES - 1) / SPE_TILES;
+    for (uint64_t task = wid; task < nchunks * ngrp; task += nwarps) {
+        const uint32_t w0 = (uint32_t)(task % ngrp) * 4;
+        const uint64_t t0 = (task / ngrp) * SPE_TILES;
+        unsigned long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (uint64_t t = t0; t < t0 + SPE_TILES && t < ntiles; ++t) {
+            const uint64_t row = t * 32 + lane;
+            uint32_t d = 0;
+            if (row < nrows) {
+                const int q = row_state(S, A.nq, row);
+                d = prod_deg(A, q, S.lo[q] + (uint32_t)(row - S.row_base[q]));
+            }
+            if (!__any_sync(0xffffffffu, d != 0)) continue;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint64_t x = (d && w0 + k < nw) ? ld_cg(Vis + row * nw + w0 + k) : 0ull;
+                if (!__any_sync(0xffffffffu, x != 0)) continue;
+#pragma unroll 8
+                for (int b = 0; b < 32; ++b) {
+                    const uint32_t s0 = __reduce_add_sync(0xffffffffu, ((x >> b) & 1ull) ? d : 0u);
+                    const uint32_t s1 = __reduce_add_sync(0xffffffffu, ((x >> (b + 32)) & 1ull) ? d : 0u);
+                    if (lane == b) { acc[2 * k] += s0; acc[2 * k + 1] += s1; }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i0 = (w0 + k) * 64 + lane, i1 = i0 + 32;
+            if (acc[2 * k] && i0 < nb) atomicAdd(pe + i0, acc[2 * k]);
+            if (acc[2 * k + 1] && i1 < nb) atomicAdd(pe + i1, acc[2 * k + 1]);
+        }
+    }
+}
+
+// per-source PE of the seeds when q0 has no rows: out-degree of (s_i, q0)
+__global__ void k_source_pe_seeds(const DevAuto A, const uint32_t *cand, const uint32_t *pidx, uint64_t b0, uint32_t nb,
+                                  unsigned long long *pe) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x)
+        pe[i] += prod_deg(A, 0, cand[pidx[b0 + i]]);
 }
 
 // PE of the seeds when q0 has no rows (k_seed_expand): out-degree of (s, q0).
@@ -899,8 +954,6 @@ __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const 
         ctrl->ucnt[0] = ctrl->ucnt[1] = 0;
         ctrl->ucur[0] = ctrl->ucur[1] = 0;
         ctrl->ntouched = 0;
-        ctrl->pull_off = 0;
-        ctrl->pull_need = ctrl->pull_done = 0;
     }
 }
 
@@ -1051,7 +1104,8 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_sparse(const DevAuto A, const
                                                           unsigned long long *stats,
                                                           const unsigned long long *start = nullptr,
                                                           uint32_t *osrc = nullptr, uint32_t *odst = nullptr,
-                                                          int *err = nullptr, const uint64_t *n_dev = nullptr) {
+                                                          int *err = nullptr, const uint64_t *n_dev = nullptr,
+                                                          unsigned long long *spe = nullptr) {
     __shared__ uint64_t tab_s[SP_WARPS][SP_H];
     if (n_dev) n = *n_dev;
     __shared__ uint64_t que_s[SP_WARPS][SP_Q];
@@ -1138,6 +1192,7 @@ __global__ void __launch_bounds__(SP_WARPS * 32) k_sparse(const DevAuto A, const
             if (lane == 0) {
                 counts[pi] = ovf ? 0ull : cnt;
                 overflow[pi] = ovf ? 1 : 0;
+                if (spe) spe[pi] = ovf ? 0ull : pe;
             }
             if (!ovf) { pe_acc += pe; src_done++; }
         }
@@ -1166,7 +1221,8 @@ __global__ void __launch_bounds__(256) k_sparse_thread(const DevAuto A, const ui
                                                        unsigned long long *counts, uint8_t *tovf,
                                                        unsigned long long *stats,
                                                        const unsigned long long *start = nullptr,
-                                                       uint32_t *osrc = nullptr, uint32_t *odst = nullptr) {
+                                                       uint32_t *osrc = nullptr, uint32_t *odst = nullptr,
+                                                       unsigned long long *spe = nullptr) {
     uint64_t lst[ST_K];
     unsigned long long pe_acc = 0, src_done = 0;
     for (uint64_t pi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; pi < n;
@@ -1229,6 +1285,7 @@ __global__ void __launch_bounds__(256) k_sparse_thread(const DevAuto A, const ui
         }
         if (!WRITE) {
             counts[pi] = cnt;
+            if (spe) spe[pi] = scanned;   // every reached key was expanded: its product edges (R12)
             if (STATS) {
                 pe_acc += scanned;   // every key was expanded: the product edges of the reach (PE, R12)
                 src_done++;
@@ -1360,6 +1417,12 @@ __global__ void k_prod_bounds(const uint64_t *d_np, const uint32_t *pidx, const 
     out[2] = np ? cand[pidx[np - 1]] : 0u;
 }
 
+__global__ void k_gather_u64(const unsigned long long *src, const uint64_t *idx, uint64_t n,
+                             unsigned long long *out) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+        out[j] = src[idx[j]];
+}
+
 __global__ void k_iota(uint32_t *x, uint64_t n) {
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
         x[j] = (uint32_t)j;
@@ -1385,28 +1448,42 @@ __device__ __forceinline__ uint64_t ans_word(const DevAuto &A, const Layout &S, 
 // A warp per vertex row: lanes over the row's words (coalesced), 4 words per
 // lane and final state loaded together so that every warp keeps several
 // sectors in flight (a streaming read of the final states' rows).
+// PE variant (pe != nullptr, RPQ_PE / RPQ_STATS): every state's row of v is
+// read once -- final rows for the count, rows with product out-degree for
+// popcount x out-degree -- so PE costs no extra pass when all states are
+// final (e.g. (a|b)*c*).  [vlo, vlo + vn) must then cover every state's range.
 __global__ void k_count_total(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
                               uint32_t nw, unsigned long long *total, const Ctrl *ctrl, uint64_t nunits,
-                              int force_dense) {
+                              int force_dense, unsigned long long *pe = nullptr) {
     if (!force_dense && ctrl && (uint64_t)ctrl->ntouched * 4 <= nunits) return;   // sparse: k_count_touched counts
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    unsigned long long acc = 0;
+    unsigned long long acc = 0, pacc = 0;
+    const uint64_t qmask = pe ? ((A.nq >= 64 ? ~0ull : ((1ull << A.nq) - 1ull))) : A.final_mask;
     for (uint64_t r = wid; r < vn; r += nwarps) {
         const uint32_t v = vlo + (uint32_t)r;
         for (uint32_t w0 = 0; w0 < nw; w0 += 128) {
             uint64_t x[4] = {0, 0, 0, 0};
-            uint64_t fm = A.final_mask;
-            while (fm) {
-                const int q = __ffsll((long long)fm) - 1;
-                fm &= fm - 1;
+            uint64_t qm = qmask;
+            while (qm) {
+                const int q = __ffsll((long long)qm) - 1;
+                qm &= qm - 1;
                 if (v - S.lo[q] >= S.len[q]) continue;
+                const bool fin = (A.final_mask >> q) & 1ull;
+                const uint32_t d = pe ? prod_deg(A, q, v) : 0u;   // offsets: L1 hits after the first pass
+                if (!fin && !d) continue;
                 const uint64_t *rp = Vis + (S.row_base[q] + (v - S.lo[q])) * nw;
+                uint64_t y[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const uint32_t w = w0 + 32u * j + lane;
-                    if (w < nw) x[j] |= ld_cg(rp + w);
+                    y[j] = w < nw ? ld_cg(rp + w) : 0ull;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (fin) x[j] |= y[j];
+                    pacc += (unsigned long long)__popcll(y[j]) * d;
                 }
             }
 #pragma unroll
@@ -1414,8 +1491,12 @@ __global__ void k_count_total(const DevAuto A, const Layout S, const uint64_t *V
         }
     }
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = 16; o; o >>= 1) {
+        acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        pacc += __shfl_xor_sync(0xffffffffu, pacc, o);
+    }
     if (lane == 0 && acc) atomicAdd(total, acc);
+    if (lane == 0 && pacc) atomicAdd(pe, pacc);
 }
 
 // Per-(source, tile) counts by warp ballot transposes: a warp takes a tile of
@@ -1489,6 +1570,11 @@ __global__ void k_scatter_counts(const unsigned long long *tot, const uint32_t *
                                  unsigned long long *cand_cnt) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x)
         cand_cnt[pidx[b0 + i]] = tot[i];
+}
+
+__global__ void k_ps_flags(const unsigned long long *cnt, const unsigned long long *pe, uint64_t n, uint8_t *flag) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x)
+        flag[j] = cnt[j] != 0 || (pe && pe[j] != 0);
 }
 
 __global__ void k_fill_eps(unsigned long long *cand_cnt, uint64_t n, unsigned long long val) {
@@ -1608,10 +1694,6 @@ struct PhaseTimer {
         }
         for (auto &e : evs) cudaEventDestroy(e.second);
     }
-};
-
-struct NZ {
-    __host__ __device__ bool operator()(const unsigned long long &x) const { return x != 0; }
 };
 
 inline int grid_for(uint64_t threads, int block = 256, int cap = 148 * 16) {
@@ -1797,6 +1879,9 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     const bool want_pairs = o.mode & RPQ_PAIRS;
     const bool want_ps = (o.mode & RPQ_PER_SOURCE) || want_pairs;
     const bool stats = o.mode & RPQ_STATS;
+    // PE (product edges traversed, reading R12) from the post-pass only, no
+    // in-kernel counters: fused into the COUNT pass (dense and touched paths)
+    const bool want_pe = stats || (o.mode & RPQ_PE);
     const bool timeit = o.mode & RPQ_TIME_KERNELS;
     const uint32_t shard_count = o.shard_count ? o.shard_count : 1;
     if (o.shard_index >= shard_count) return rpq_fail(RPQ_EINVAL, "shard_index >= shard_count");
@@ -1807,6 +1892,8 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     Workspace ws{s, {}};
 
     rpq_result *res = new rpq_result();
+    res->stream = (void *)s;
+    res->alloc_snap = alloc_snapshot();
     res->device = g->device;
     auto fail = [&](rpq_status st) { rpq_result_release(res); return st; };
     cudaEvent_t evt0, evt1, e_begin, e_end;
@@ -1959,6 +2046,18 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         if (q == 0 && np && !skip_q0) r = hull(r, Range{p_first, p_last});
         R_max += r.empty() ? 0 : (uint64_t)r.hi - r.lo + 1;
     }
+    // global row indices (state, vertex) are u32 inside the level kernels
+    if (R_max >= (1ull << 32))
+        return fail(rpq_fail(RPQ_EUNSUPPORTED, "%llu state rows (sum of per-state vertex ranges) >= 2^32",
+                             (unsigned long long)R_max));
+    // Sharded evaluations must cut the sources into the SAME batches on every
+    // rank (batch b -> shard b % shard_count): the automatic width depends on
+    // this device's free memory, so it is only allowed with an explicit
+    // budget; rpq_plan + an all-reduce MIN (rpq_eval_allpairs_dist in the
+    // Python layer) agrees on one width.
+    if (shard_count > 1 && o.batch_sources == 0 && o.hbm_budget_bytes == 0 && !(o.reserved & 4u))
+        return fail(rpq_fail(RPQ_EINVAL, "shard_count > 1 needs batch_sources or hbm_budget_bytes (ranks must agree "
+                                         "on the batch plan; see rpq_plan)"));
     uint64_t budget = o.hbm_budget_bytes ? o.hbm_budget_bytes : (uint64_t)(dev_available(budget_cached) * 0.9);
     HM("dev_available");
     uint64_t B = o.batch_sources;
@@ -1983,6 +2082,11 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         uint64_t nw_max = per_word > 0 ? (uint64_t)(bud / per_word) : 1;
         if (nw_max < 1) nw_max = 1;
         B = std::min<uint64_t>(std::max<uint64_t>(np, 1), nw_max * 64);
+        // shard-aware: at least one batch per shard, widths in whole words
+        if (shard_count > 1) {
+            const uint64_t per = ((np + shard_count - 1) / shard_count + 63) / 64 * 64;
+            B = std::min<uint64_t>(B, std::max<uint64_t>(per, 64));
+        }
     }
     B = std::max<uint64_t>(1, B);
     uint64_t nw = (B + 63) / 64;
@@ -2002,6 +2106,12 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     const uint64_t nbatches = np ? (np + B - 1) / B : 0;
     ST.batch_sources = (uint32_t)B;
     ST.chunk_words = CW;
+    if (o.reserved & 4u) {   // rpq_plan: the batch plan only, nothing evaluated
+        ST.batches = (uint32_t)nbatches;
+        ST.state_words = R_max * nw;
+        *out = res;
+        return RPQ_OK;
+    }
 
     // batch boundaries: first/last productive candidate index of each batch
     // and their vertex ids (one kernel + one copy for all batches)
@@ -2033,6 +2143,16 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     uint64_t sparse_total = 0, sub_pe = 0;
     rpq_result *sub_keep = nullptr;
     unsigned long long *cand_cnt = nullptr;
+    // RPQ_SOURCE_PE: per-candidate product edges (verification mode)
+    const bool want_spe = want_ps && (o.mode & RPQ_SOURCE_PE);
+    unsigned long long *cand_pe = nullptr, *spe = nullptr;
+    if (want_spe) {
+        cand_pe = (unsigned long long *)ws.get(std::max<uint64_t>(nsrc, 1) * 8);
+        spe = (unsigned long long *)ws.get(std::max<uint64_t>(np, 1) * 8);
+        if (!cand_pe || !spe) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (per-source PE)"));
+        RPQ_CUDA_TRY(cudaMemsetAsync(cand_pe, 0, std::max<uint64_t>(nsrc, 1) * 8, s));
+        RPQ_CUDA_TRY(cudaMemsetAsync(spe, 0, std::max<uint64_t>(np, 1) * 8, s));
+    }
     unsigned long long *d_stats = (unsigned long long *)ws.get(NSTAT * 8 + 8);
     if (!d_stats) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
     unsigned long long *d_total = d_stats + NSTAT;
@@ -2077,12 +2197,14 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                 // thread tier over every source of the shard, then the warp
                 // tier over the sources the thread tier could not hold
                 RPQ_CUDA_TRY(cudaMemsetAsync(tov, 0, np, s));
-                if (stats)
+                if (want_pe)
                     k_sparse_thread<true, false><<<grid_for(np), 256, 0, s>>>(A, cand, pidx, np, B, o.shard_index,
-                                                                             shard_count, sc, tov, d_stats);
+                                                                             shard_count, sc, tov, d_stats, nullptr,
+                                                                             nullptr, nullptr, spe);
                 else
                     k_sparse_thread<false, false><<<grid_for(np), 256, 0, s>>>(A, cand, pidx, np, B, o.shard_index,
-                                                                              shard_count, sc, tov, d_stats);
+                                                                              shard_count, sc, tov, d_stats, nullptr,
+                                                                              nullptr, nullptr, spe);
                 {
                     size_t tt = 0;
                     thrust::counting_iterator<uint32_t> itt(0);
@@ -2091,14 +2213,14 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                     if (!tmpt) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
                     cub::DeviceSelect::Flagged(tmpt, tt, itt, tov, tlist, d_nt, (int64_t)np, s);
                 }
-                if (stats)
+                if (want_pe)
                     k_sparse<true, false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, tlist, np, B, o.shard_index,
                                                                      shard_count, sc, sov, d_stats, nullptr, nullptr,
-                                                                     nullptr, nullptr, d_nt);
+                                                                     nullptr, nullptr, d_nt, spe);
                 else
                     k_sparse<false, false><<<148 * 8, SP_WARPS * 32, 0, s>>>(A, cand, pidx, tlist, np, B, o.shard_index,
                                                                       shard_count, sc, sov, d_stats, nullptr, nullptr,
-                                                                      nullptr, nullptr, d_nt);
+                                                                      nullptr, nullptr, d_nt, spe);
                 ST.kernel_launches += 3;
                 if (timeit) {
                     cudaEventRecord(sp1, s);
@@ -2141,6 +2263,9 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                     k_fill_eps<<<grid_for(nsrc), 256, 0, s>>>(cand_cnt, nsrc, eps ? 1ull : 0ull);
                     k_sparse_scatter<<<grid_for(np), 256, 0, s>>>(pidx, sc, sov, np, B, o.shard_index, shard_count,
                                                                  cand_cnt);
+                    if (want_spe)
+                        k_sparse_scatter<<<grid_for(np), 256, 0, s>>>(pidx, spe, sov, np, B, o.shard_index,
+                                                                     shard_count, cand_pe);
                     ST.kernel_launches += 2;
                 }
                 if (no) {
@@ -2152,7 +2277,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                     so.reserved |= 1u;               // dense only
                     so.shard_index = 0;
                     so.shard_count = 1;
-                    so.mode = (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS)) |
+                    so.mode = (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS | RPQ_PE | RPQ_SOURCE_PE)) |
                               (want_pairs ? RPQ_PAIRS : want_ps ? RPQ_PER_SOURCE : RPQ_COUNT);
                     rpq_result *sub = nullptr;
                     rpq_status sst = eval_sources_device(g, a, osrc, no, &so, &sub);
@@ -2169,6 +2294,9 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                     if (want_ps && sub->n_ps) {
                         k_scatter_sub<<<grid_for(sub->n_ps), 256, 0, s>>>(
                             cand, nsrc, sub->ps_src, (const unsigned long long *)sub->ps_cnt, sub->n_ps, cand_cnt);
+                        if (want_spe && sub->ps_pe)
+                            k_scatter_sub<<<grid_for(sub->n_ps), 256, 0, s>>>(
+                                cand, nsrc, sub->ps_src, (const unsigned long long *)sub->ps_pe, sub->n_ps, cand_pe);
                         ST.kernel_launches++;
                     }
                     if (want_pairs) {   // keep the sub-result until its pairs are placed
@@ -2195,6 +2323,26 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                     RPQ_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int), s));
                     RPQ_CUDA_TRY(cudaStreamSynchronize(s));
                     const uint64_t tot = ls + lc;
+                    {   // per-batch row ranges of this shard (start = global scan, other shards zeroed)
+                        std::vector<uint64_t> bj;
+                        for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count) bj.push_back(b);
+                        if (!bj.empty()) {
+                            std::vector<unsigned long long> hs(bj.size());
+                            unsigned long long *d_bs = (unsigned long long *)ws.get(bj.size() * 8);
+                            uint64_t *d_bj = (uint64_t *)ws.get(bj.size() * 8);
+                            if (!d_bs || !d_bj) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                            for (auto &x : bj) x = js[x];
+                            RPQ_CUDA_TRY(cudaMemcpyAsync(d_bj, bj.data(), bj.size() * 8, cudaMemcpyHostToDevice, s));
+                            k_gather_u64<<<grid_for(bj.size()), 256, 0, s>>>(start, d_bj, bj.size(), d_bs);
+                            RPQ_CUDA_TRY(cudaMemcpyAsync(hs.data(), d_bs, bj.size() * 8, cudaMemcpyDeviceToHost, s));
+                            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                            size_t k = 0;
+                            for (uint64_t b = o.shard_index; b < nb_eff; b += shard_count, ++k) {
+                                const uint64_t hi = k + 1 < hs.size() ? hs[k + 1] : tot;
+                                res->batches.push_back(rpq_batch_info{js[b], js[b + 1], hs[k], hi - hs[k]});
+                            }
+                        }
+                    }
                     res->ncols = 2;
                     res->nrows = tot;
                     if (!dev_alloc_to(res->cols[0], std::max<uint64_t>(tot, 1) * 4, s) ||
@@ -2401,11 +2549,11 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
 
     // layouts of this shard's batches, computed up front and copied once
     std::vector<Layout> lay_h;
-    std::vector<Range> lay_fin;
+    std::vector<Range> lay_fin, lay_all;
     for (uint64_t b = o.shard_index; b < (sparse_done ? 0 : nbatches); b += shard_count) {
         Layout S{};
         uint64_t rows = 0;
-        Range fin_hull{1, 0};
+        Range fin_hull{1, 0}, all_hull{1, 0};
         for (uint32_t q = 0; q < a->nq; ++q) {
             Range r = in_range[q];
             if (q == 0 && !skip_q0) r = hull(r, Range{sfirst[b], slast[b]});
@@ -2414,9 +2562,11 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             S.len[q] = r.empty() ? 0 : r.hi - r.lo + 1;
             rows += S.len[q];
             if ((a->final_mask >> q) & 1) fin_hull = hull(fin_hull, r);
+            all_hull = hull(all_hull, r);
         }
         lay_h.push_back(S);
         lay_fin.push_back(fin_hull);
+        lay_all.push_back(all_hull);
     }
     Layout *d_layouts = (Layout *)ws.get(std::max<size_t>(lay_h.size(), 1) * sizeof(Layout));
     if (!d_layouts) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
@@ -2446,6 +2596,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         ST.batches++;
         if (b >= nbatches) {   // virtual batch: only epsilon pairs
             const uint64_t ne = eps ? (jhi - jlo) : 0;
+            if (want_ps) res->batches.push_back(rpq_batch_info{jlo, jhi, total, ne});
             total += ne;
             if (want_pairs && ne) {
                 Block bl{nullptr, nullptr, ne};
@@ -2513,10 +2664,19 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         PT.mark("levels");
         HM("levels enqueued");
         if (st != RPQ_OK) return fail(st);
-        if (stats) {   // PE after the fact (exact for push and pull levels alike)
-            k_pe_rows<<<148 * 8, 256, 0, s>>>(A, S, Vis, (uint32_t)nw, d_stats + S_PE_POST);
+        if (want_spe) {   // per-source PE of this batch -> cand_pe
+            unsigned long long *bpe = (unsigned long long *)ws.get((uint64_t)nb * 8);
+            if (!bpe) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+            RPQ_CUDA_TRY(cudaMemsetAsync(bpe, 0, (uint64_t)nb * 8, s));
+            k_source_pe<<<148 * 8, 256, 0, s>>>(A, S, Vis, (uint32_t)nw, nb, bpe);
+            if (skip_q0) k_source_pe_seeds<<<grid_for(nb), 256, 0, s>>>(A, cand, pidx, b0, nb, bpe);
+            k_scatter_counts<<<grid_for(nb), 256, 0, s>>>(bpe, pidx, b0, nb, cand_pe);
+            ST.kernel_launches += skip_q0 ? 3 : 2;
+        }
+        if (want_pe) {   // PE after the fact (exact for push and pull levels alike)
+            if (want_ps) k_pe_rows<<<148 * 8, 256, 0, s>>>(A, S, Vis, (uint32_t)nw, d_stats + S_PE_POST);
             if (skip_q0) k_pe_seeds<<<grid_for(nb), 256, 0, s>>>(A, cand, pidx, b0, nb, d_stats + S_PE_POST);
-            ST.kernel_launches += skip_q0 ? 2 : 1;
+            ST.kernel_launches += (want_ps ? 1 : 0) + (skip_q0 ? 1 : 0);
         }
         // X and XB are all zero again here (the last level activated
         // nothing).  Extraction reads Vis of the final states.
@@ -2525,11 +2685,16 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         const uint64_t eps_np = eps ? (jhi - jlo) - nb : 0;   // non-productive candidates in the interval
         if (!want_ps) {
             // COUNT: accumulate on the device (sparse or dense path chosen
-            // there from the touched-unit count); no host round trip
-            k_count_touched<<<148 * 8, 256, 0, s>>>(A, S, P0, nunits, d_total, dead_final);
-            if (vn) k_count_total<<<grid_for(vn * 32), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, d_total, ctrl,
-                                                                     nunits, dead_final);
-            ST.kernel_launches += vn ? 2 : 1;
+            // there from the touched-unit count); no host round trip.  With
+            // PE the count pass reads every state's rows (hull of all ranges).
+            const Range all_hull = lay_all[lay_i - 1];
+            const uint32_t clo = want_pe ? (all_hull.empty() ? 0 : all_hull.lo) : vlo;
+            const uint64_t cn = want_pe ? (all_hull.empty() ? 0 : (uint64_t)all_hull.hi - all_hull.lo + 1) : vn;
+            unsigned long long *pe_out = want_pe ? d_stats + S_PE_POST : nullptr;
+            k_count_touched<<<148 * 8, 256, 0, s>>>(A, S, P0, nunits, d_total, dead_final, pe_out);
+            if (cn) k_count_total<<<grid_for(cn * 32), 256, 0, s>>>(A, S, Vis, clo, cn, (uint32_t)nw, d_total, ctrl,
+                                                                     nunits, dead_final, pe_out);
+            ST.kernel_launches += cn ? 2 : 1;
             total += eps_np;
             continue;
         }
@@ -2560,6 +2725,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         RPQ_CUDA_TRY(cudaMemcpyAsync(&last_cnt, cand_cnt + jhi - 1, 8, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
         const uint64_t bt = last_start + last_cnt;
+        res->batches.push_back(rpq_batch_info{jlo, jhi, total, bt});
         total += bt;
         if (want_pairs && bt) {
             Block bl{nullptr, nullptr, bt};
@@ -2630,6 +2796,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             if (b % shard_count != o.shard_index) {
                 uint64_t jl = jstart(b), jh = (b + 1 < nb_eff) ? jstart(b + 1) : nsrc;
                 if (jh > jl) RPQ_CUDA_TRY(cudaMemsetAsync(cand_cnt + jl, 0, (jh - jl) * 8, s));
+                if (jh > jl && want_spe) RPQ_CUDA_TRY(cudaMemsetAsync(cand_pe + jl, 0, (jh - jl) * 8, s));
             }
         uint8_t *nz = (uint8_t *)ws.get(nsrc);
         uint64_t *d_n = (uint64_t *)ws.get(8);
@@ -2638,13 +2805,21 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             cudaGetLastError();
             return fail(rpq_fail(RPQ_ENOMEM, "oom"));
         }
+        if (want_spe && !dev_alloc_to(res->ps_pe, nsrc * 8, s)) {
+            cudaGetLastError();
+            return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+        }
+        // listed: non-zero count (or, with RPQ_SOURCE_PE, non-zero PE)
+        k_ps_flags<<<grid_for(nsrc), 256, 0, s>>>(cand_cnt, want_spe ? cand_pe : nullptr, nsrc, nz);
         size_t tb1 = 0, tb2 = 0;
-        cub::DeviceSelect::If(nullptr, tb1, cand_cnt, (unsigned long long *)res->ps_cnt, d_n, (int64_t)nsrc, NZ(), s);
-        cub::DeviceSelect::FlaggedIf(nullptr, tb2, cand, cand_cnt, res->ps_src, d_n, (int64_t)nsrc, NZ(), s);
+        cub::DeviceSelect::Flagged(nullptr, tb1, cand_cnt, nz, (unsigned long long *)res->ps_cnt, d_n, (int64_t)nsrc, s);
+        cub::DeviceSelect::Flagged(nullptr, tb2, cand, nz, res->ps_src, d_n, (int64_t)nsrc, s);
         void *tmp = ws.get(std::max(tb1, tb2));
         if (!tmp) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
-        cub::DeviceSelect::If(tmp, tb1, cand_cnt, (unsigned long long *)res->ps_cnt, d_n, (int64_t)nsrc, NZ(), s);
-        cub::DeviceSelect::FlaggedIf(tmp, tb2, cand, cand_cnt, res->ps_src, d_n, (int64_t)nsrc, NZ(), s);
+        cub::DeviceSelect::Flagged(tmp, tb1, cand_cnt, nz, (unsigned long long *)res->ps_cnt, d_n, (int64_t)nsrc, s);
+        if (want_spe)
+            cub::DeviceSelect::Flagged(tmp, tb1, cand_pe, nz, (unsigned long long *)res->ps_pe, d_n, (int64_t)nsrc, s);
+        cub::DeviceSelect::Flagged(tmp, tb2, cand, nz, res->ps_src, d_n, (int64_t)nsrc, s);
         RPQ_CUDA_TRY(cudaMemcpyAsync(&res->n_ps, d_n, 8, cudaMemcpyDeviceToHost, s));
     }
     if (nbatches && !sparse_done) {
@@ -2656,7 +2831,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             ST.kernel_launches += (2ull + (need_hub ? 1 : 0) + (P0.pull_mode ? 2 : 0)) * hc.levels + (hc.levels + 1) / 2;
         ST.expand_launches = 2ull * ST.levels;
     }
-    if (stats) {
+    if (stats || want_pe) {
         unsigned long long hs[NSTAT];
         RPQ_CUDA_TRY(cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
@@ -2715,6 +2890,24 @@ extern "C" rpq_status rpq_eval_allpairs(const rpq_graph *g, const rpq_nfa *a, co
     return eval_sources_device(g, a, nullptr, 0, opts, out);
 }
 
+extern "C" rpq_status rpq_plan(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
+                               rpq_plan_info *info) {
+    if (!g || !a || !info) return rpq_fail(RPQ_EINVAL, "NULL argument");
+    rpq_eval_opts o{};
+    if (opts) o = *opts;
+    o.reserved |= 4u;
+    rpq_result *r = nullptr;
+    rpq_status st = eval_sources_device(g, a, nullptr, 0, &o, &r);
+    if (st != RPQ_OK) return st;
+    info->productive_sources = r->stats.productive_sources;
+    info->batch_sources = r->stats.batch_sources;
+    info->num_batches = r->stats.batches;
+    info->state_words = r->stats.state_words;
+    info->chunk_words = r->stats.chunk_words;
+    rpq_result_release(r);
+    return RPQ_OK;
+}
+
 extern "C" rpq_status rpq_eval_sources(const rpq_graph *g, const rpq_nfa *a, const uint32_t *srcs, uint64_t n,
                                        const rpq_eval_opts *opts, rpq_result **out) {
     rpq_status st = check_common(g, a, out);
@@ -2751,6 +2944,9 @@ extern "C" rpq_status rpq_eval_allpairs_stream(const rpq_graph *g, const rpq_nfa
     if (opts) o = *opts;
     const uint32_t shard_count = o.shard_count ? o.shard_count : 1;
     if (o.shard_index >= shard_count) return rpq_fail(RPQ_EINVAL, "shard_index >= shard_count");
+    // chunk boundaries follow the device budget: ranks must pass the same one
+    if (shard_count > 1 && !device_budget_bytes)
+        return rpq_fail(RPQ_EINVAL, "sharded streaming needs an explicit device_budget_bytes (same on every rank)");
     RPQ_CUDA_TRY(cudaSetDevice(g->device));
     cudaStream_t s = (cudaStream_t)o.cuda_stream;
     if (!piece_pairs) piece_pairs = 1ull << 26;

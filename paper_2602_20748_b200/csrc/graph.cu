@@ -96,14 +96,32 @@ struct Cleanup {
 
 }  // namespace
 
+// Long-lived graph blocks: the caller's allocator when one was installed at
+// load time (rpq_set_allocator), else plain cudaMalloc (not the stream pool:
+// the graph outlives every stream the caller may use).
+static void *graph_alloc(const rpq_graph *g, size_t bytes, cudaStream_t s) {
+    if (g->alloc_snap && g->alloc_snap->alloc) return g->alloc_snap->alloc(bytes, (void *)s, g->alloc_snap->ctx);
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    return p;
+}
+
+static void graph_block_free(const rpq_graph *g, void *p) {
+    if (!p) return;
+    if (g->alloc_snap && g->alloc_snap->free_) g->alloc_snap->free_(p, nullptr, g->alloc_snap->ctx);
+    else cudaFree(p);
+}
+
 extern "C" void rpq_graph_free(rpq_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
+    cudaDeviceSynchronize();         // no evaluation may still read the CSR
     for (int p = 0; p < 2; ++p) {    // label CSRs are slices of these blocks
-        if (g->off_base[p]) cudaFree(g->off_base[p]);
-        if (g->nbr_base[p]) cudaFree(g->nbr_base[p]);
+        graph_block_free(g, g->off_base[p]);
+        graph_block_free(g, g->nbr_base[p]);
     }
-    if (g->vlabel) cudaFree(g->vlabel);
+    graph_block_free(g, g->vlabel);
+    delete g->alloc_snap;
     delete g;
     dev_available_invalidate();
 }
@@ -155,9 +173,15 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
     RPQ_CUDA_TRY(cudaMemcpyAsync(cnt.data(), d_cnt, nl * 8ull, cudaMemcpyDeviceToHost, s));
     RPQ_CUDA_TRY(cudaStreamSynchronize(s));
     if (bad) return rpq_fail(RPQ_EINVAL, "rpq_graph_load: vertex id >= num_vertices or label >= num_labels");
+    // per-label offsets and CSR edge indices are u32 (internal.h LabelCSR)
+    for (uint32_t l = 0; l < nl; ++l)
+        if (cnt[l] > 0xffffffffull)
+            return rpq_fail(RPQ_EUNSUPPORTED, "rpq_graph_load: label %u has %llu >= 2^32 edges (u32 CSR offsets)", l,
+                            (unsigned long long)cnt[l]);
     std::vector<unsigned long long> start(nl + 1, 0);
     for (uint32_t l = 0; l < nl; ++l) start[l + 1] = start[l] + cnt[l];
     rpq_graph *g = new rpq_graph();
+    g->alloc_snap = alloc_snapshot();
     g->device = d->device;
     g->nv = nv;
     for (uint32_t l = 0; l < nl; ++l) g->label_names.emplace_back(d->label_names[l] ? d->label_names[l] : "");
@@ -167,6 +191,16 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
     int vbits = 1;
     while (vbits < 32 && (1ull << vbits) < nv) ++vbits;
     auto fail = [&](rpq_status st, const char *m) { rpq_graph_free(g); return rpq_fail(st, "rpq_graph_load: %s", m); };
+    // CUDA errors after g exists free it (and its CSR blocks) before returning
+#define GTRY(expr)                                                                               \
+    do {                                                                                         \
+        cudaError_t _e = (expr);                                                                 \
+        if (_e != cudaSuccess) {                                                                 \
+            char _m[512];                                                                        \
+            snprintf(_m, sizeof(_m), "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+            return fail(_e == cudaErrorMemoryAllocation ? RPQ_ENOMEM : RPQ_ECUDA, _m);           \
+        }                                                                                        \
+    } while (0)
 
     // pass 0: out-edge CSR (keys u<<32|w); pass 1 (RPQ_GRAPH_IN_EDGES): the
     // in-edge CSR of the transposed graph (keys w<<32|u), same construction.
@@ -195,25 +229,23 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
     void *tstore = alloc(std::max<size_t>(tbytes, 16));
     if (!tstore) return fail(RPQ_ENOMEM, "sort temp");
     for (int pass = 0; pass < (in_edges ? 2 : 1); ++pass) {
-        RPQ_CUDA_TRY(cudaMemcpyAsync(d_cnt, start.data(), nl * 8ull, cudaMemcpyHostToDevice, s));
+        GTRY(cudaMemcpyAsync(d_cnt, start.data(), nl * 8ull, cudaMemcpyHostToDevice, s));
         if (ne) {
             if (pass == 0) k_scatter<<<grid_for(ne), 256, 0, s>>>(d_src, d_dst, d_lab, ne, d_cnt, keys);
             else k_scatter<<<grid_for(ne), 256, 0, s>>>(d_dst, d_src, d_lab, ne, d_cnt, keys);
         }
-        RPQ_CUDA_TRY(cudaGetLastError());
+        GTRY(cudaGetLastError());
         std::vector<LabelCSR> &csrs = pass == 0 ? g->csr : g->in_csr;
         uint32_t *&off_all = g->off_base[pass];
         uint32_t *&nbr_all = g->nbr_base[pass];
-        if (cudaMalloc(&off_all, (uint64_t)nl * (nv + 1ull) * 4) != cudaSuccess ||
-            cudaMalloc(&nbr_all, std::max<uint64_t>(nstart[nl], 4) * 4) != cudaSuccess) {
-            cudaGetLastError();
-            return fail(RPQ_ENOMEM, "CSR arrays");
-        }
-        RPQ_CUDA_TRY(cudaMemsetAsync(off_all, 0, (uint64_t)nl * (nv + 1ull) * 4, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(d_m, 0, nl * 8ull, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(d_fl, 0, nl * 16ull, s));
-        RPQ_CUDA_TRY(cudaMemsetAsync(d_mm, 0xff, nl * 8ull, s));   // (min, max) = (~0, ~0): max fixed below
-        RPQ_CUDA_TRY(cudaMemsetAsync(d_md, 0, nl * 4ull, s));
+        off_all = (uint32_t *)graph_alloc(g, (uint64_t)nl * (nv + 1ull) * 4, s);
+        nbr_all = (uint32_t *)graph_alloc(g, std::max<uint64_t>(nstart[nl], 4) * 4, s);
+        if (!off_all || !nbr_all) return fail(RPQ_ENOMEM, "CSR arrays");
+        GTRY(cudaMemsetAsync(off_all, 0, (uint64_t)nl * (nv + 1ull) * 4, s));
+        GTRY(cudaMemsetAsync(d_m, 0, nl * 8ull, s));
+        GTRY(cudaMemsetAsync(d_fl, 0, nl * 16ull, s));
+        GTRY(cudaMemsetAsync(d_mm, 0xff, nl * 8ull, s));   // (min, max) = (~0, ~0): max fixed below
+        GTRY(cudaMemsetAsync(d_md, 0, nl * 4ull, s));
         for (uint32_t l = 0; l < nl; ++l) {
             LabelCSR &c = csrs[l];
             c.off = off_all + (uint64_t)l * (nv + 1ull);
@@ -222,7 +254,7 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
             if (n == 0) continue;
             uint64_t *kin = keys + start[l], *kout = keys2 + start[l];
             size_t tb = tbytes;
-            RPQ_CUDA_TRY(cudaMemsetAsync(d_mm + 2 * l + 1, 0, 4, s));
+            GTRY(cudaMemsetAsync(d_mm + 2 * l + 1, 0, 4, s));
             cub::DeviceRadixSort::SortKeys(tstore, tb, kin, kout, (int64_t)n, 0, 32 + vbits, s);
             tb = tbytes;
             cub::DeviceSelect::Unique(tstore, tb, kout, kin, d_m + l, (int64_t)n, s);
@@ -233,11 +265,11 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
         }
         std::vector<uint64_t> hm(nl), hfl(2 * nl);
         std::vector<uint32_t> hmm(2 * nl), hmd(nl);
-        RPQ_CUDA_TRY(cudaMemcpyAsync(hmd.data(), d_md, nl * 4ull, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaMemcpyAsync(hm.data(), d_m, nl * 8ull, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaMemcpyAsync(hfl.data(), d_fl, nl * 16ull, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaMemcpyAsync(hmm.data(), d_mm, nl * 8ull, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        GTRY(cudaMemcpyAsync(hmd.data(), d_md, nl * 4ull, cudaMemcpyDeviceToHost, s));
+        GTRY(cudaMemcpyAsync(hm.data(), d_m, nl * 8ull, cudaMemcpyDeviceToHost, s));
+        GTRY(cudaMemcpyAsync(hfl.data(), d_fl, nl * 16ull, cudaMemcpyDeviceToHost, s));
+        GTRY(cudaMemcpyAsync(hmm.data(), d_mm, nl * 8ull, cudaMemcpyDeviceToHost, s));
+        GTRY(cudaStreamSynchronize(s));
         for (uint32_t l = 0; l < nl; ++l) {
             LabelCSR &c = csrs[l];
             c.m = cnt[l] ? hm[l] : 0;
@@ -255,14 +287,16 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
             for (uint32_t i = 0; i < d->num_vertex_labels; ++i)
                 g->vlabel_names.emplace_back(d->vertex_label_names[i] ? d->vertex_label_names[i] : "");
         g->h_vlabel.assign(d->vertex_label, d->vertex_label + nv);
-        if (cudaMalloc(&g->vlabel, nv * 2ull) != cudaSuccess) { cudaGetLastError(); return fail(RPQ_ENOMEM, "vertex labels"); }
-        RPQ_CUDA_TRY(cudaMemcpyAsync(g->vlabel, d->vertex_label, nv * 2ull, cudaMemcpyHostToDevice, s));
+        g->vlabel = (uint16_t *)graph_alloc(g, nv * 2ull, s);
+        if (!g->vlabel) return fail(RPQ_ENOMEM, "vertex labels");
+        GTRY(cudaMemcpyAsync(g->vlabel, d->vertex_label, nv * 2ull, cudaMemcpyHostToDevice, s));
     }
     cudaError_t e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return fail(RPQ_ECUDA, cudaGetErrorString(e));
     *out = g;
     dev_available_invalidate();
     return RPQ_OK;
+#undef GTRY
 }
 
 extern "C" rpq_status rpq_graph_info(const rpq_graph *g, uint32_t *nv, uint64_t *ne, uint32_t *nl) {

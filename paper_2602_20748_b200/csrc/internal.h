@@ -40,6 +40,9 @@ struct rpq_graph {
     // -1 = not checked yet; filled lazily by label_symmetric (eval.cu)
     mutable std::mutex sym_mu;
     mutable std::vector<int8_t> sym;
+    // allocator the CSR blocks came from (rpq_set_allocator at load time;
+    // null functions = cudaMalloc / cudaFree)
+    struct AllocSnap *alloc_snap = nullptr;
 };
 
 // ---- automaton ("automata plan") ------------------------------
@@ -64,13 +67,30 @@ struct rpq_result {
     // RPQ_PER_SOURCE: non-zero (source, count), ascending source (device)
     uint32_t *ps_src = nullptr;
     uint64_t *ps_cnt = nullptr;
+    uint64_t *ps_pe = nullptr;       // RPQ_SOURCE_PE: product edges per listed source (PE, reading R12)
     uint64_t n_ps = 0;
     rpq_stats stats{};
+    // PAIRS / PER_SOURCE: this shard's batches in evaluation order (rows of
+    // batch k are [offset, offset + count) of the result)
+    std::vector<rpq_batch_info> batches;
+    // buffers are freed on the stream they were allocated on, through the
+    // allocator that was installed when they were allocated
+    void *stream = nullptr;
+    struct AllocSnap *alloc_snap = nullptr;
 };
 
 // ---- device memory (stream-ordered pool allocator) -----------------------
 void *dev_alloc(size_t bytes, void *stream);          // nullptr on failure
 void dev_free(void *p, void *stream);
+// the allocator installed right now (rpq_set_allocator), captured by objects
+// that outlive a call; freed with the same functions later
+struct AllocSnap {
+    void *(*alloc)(size_t, void *, void *) = nullptr;
+    void (*free_)(void *, void *, void *) = nullptr;
+    void *ctx = nullptr;
+};
+AllocSnap *alloc_snapshot();                          // new'd copy of the current allocator
+void dev_free_snap(void *p, void *stream, const AllocSnap *snap);
 template <class T>
 inline bool dev_alloc_to(T *&p, size_t bytes, void *stream) {
     p = static_cast<T *>(dev_alloc(bytes, stream));

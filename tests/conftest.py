@@ -35,3 +35,22 @@ def golden_int_tuples(name):
 def toy():
     import synth
     return synth.toy_graph()
+
+
+def device_rows(r, off, n):
+    """Rows [off, off + n) of a device-resident pair result, copied to the
+    host as an (n, 2) uint32 array without copying the whole result (tests
+    slice 10-100 GB PAIRS results this way)."""
+    import torch
+    from paper_2602_20748_b200.dist import _CudaBuf
+    ptrs, tot = r.device_view()
+    assert off + n <= tot
+    if n == 0:
+        return np.zeros((0, 2), np.uint32)
+    cols = [torch.as_tensor(_CudaBuf(p, tot), device="cuda")[off:off + n].cpu().numpy() for p in ptrs]
+    return np.stack(cols, 1).view(np.uint32)
+
+
+def sorted_pairs(src, dst):
+    p = np.stack([np.asarray(src), np.asarray(dst)], 1).astype(np.uint32)
+    return p[np.lexsort((p[:, 1], p[:, 0]))] if len(p) else p.reshape(0, 2)

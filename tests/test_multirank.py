@@ -110,3 +110,68 @@ def test_shard_plan_properties():
             assert (own == 0).all()
         else:
             assert (own[:pidx[0] + 1] == 0).all()          # leading non-productive -> batch 0
+
+
+def _dist_worker(rank, world, port, rx, B, out_q):
+    """The product's multi-GPU gather (paper_2602_20748_b200.dist) on gloo:
+    each rank holds the rows of its batches (here from the oracle: no GPU on
+    this box) and its batch table; rank 0 gathers them into global order."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2602_20748_b200 import dist as D
+    g = synth.random_graph(600, 2400, 3, seed=31)
+    pidx = productive(g, rx)
+    nb = -(-len(pidx) // B) if len(pidx) else 1
+    js = [0] + [int(pidx[k * B]) for k in range(1, nb)] + [g.num_vertices]
+    og = oracle.OracleGraph(g)
+    rows, table, off = [], [], 0
+    for k in range(rank, nb, world):
+        srcs = np.arange(js[k], js[k + 1], dtype=np.uint32)
+        r = oracle.eval_sources(og, rx, srcs, threads=2)
+        p = np.stack([r["src"], r["dst"]], 1).astype(np.uint32)
+        p = p[np.lexsort((p[:, 1], p[:, 0]))]
+        rows.append(p)
+        table.append((js[k], js[k + 1], off, len(p)))
+        off += len(p)
+    local = np.concatenate(rows) if rows else np.zeros((0, 2), np.uint32)
+    t = torch.from_numpy(local.view(np.int32).T.copy())
+    agreed = D.agree_batch_sources(64 * (rank + 1))
+    got = D.gather_rows_to_root(t, np.array(table, np.uint64).reshape(-1, 4))
+    parts = D.allgather_var(local[:, 0].copy())
+    if rank == 0:
+        out_q.put((agreed, got.numpy().view(np.uint32).T.copy(), [len(x) for x in parts]))
+    else:
+        assert got is None
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rx,B", [("(a|b)*c*", 64), ("a b* c", 100)])
+def test_dist_gather_rows_in_global_order(rx, B):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, rx, B, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    agreed, got, sizes = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = synth.random_graph(600, 2400, 3, seed=31)
+    o = oracle.allpairs(g, rx)
+    want = np.stack([o["src"], o["dst"]], 1).astype(np.uint32)
+    want = want[np.lexsort((want[:, 1], want[:, 0]))]
+    assert agreed == 64                       # all-reduce MIN of the per-rank widths
+    assert np.array_equal(got, want)          # every rank's blocks at their global offsets
+    assert sum(sizes) == len(want) and min(sizes) > 0
+
+
+def test_dist_placement_rejects_overlap():
+    from paper_2602_20748_b200 import dist as D
+    tot, pl = D.placement([np.array([[0, 10, 0, 5], [20, 30, 5, 2]], np.uint64),
+                           np.array([[10, 20, 0, 4]], np.uint64)])
+    assert tot == 11 and pl == [(0, 0, 0, 5), (1, 0, 5, 4), (0, 5, 9, 2)]
+    with pytest.raises(ValueError):
+        D.placement([np.array([[0, 10, 0, 5]], np.uint64), np.array([[5, 20, 0, 4]], np.uint64)])
