@@ -212,8 +212,9 @@ def pair_set(res) -> set:
 
 
 # ==========================================================================
-# Shared tokeniser for the Python oracles (reading R3: longest match; '.',
-# '/' and whitespace are optional concatenation; R2 dialects)
+# O3's tokeniser (reading R3: longest match; '.', '/' and whitespace are
+# optional concatenation; R2 dialects).  O2 has its own (below): the three
+# oracles share no code.
 # ==========================================================================
 _OPS = "()|*+?"
 
@@ -241,18 +242,41 @@ def tokenize(regex: str, names: Sequence[str]) -> List[Tuple[str, object]]:
 # ==========================================================================
 # O2: brute force over walks (Definition 1)
 # ==========================================================================
+def _o2_label_pattern(names: Sequence[str]):
+    """O2's own scanner (reading R3): one Python ``re`` alternation of the
+    label names, longest names first, so that ``re`` performs the longest
+    match at every position (e.g. 'replyOf' before 'reply')."""
+    order = sorted((k for k, n in enumerate(names) if n), key=lambda k: -len(names[k]))
+    return order, re.compile("|".join(re.escape(names[k]) for k in order)) if order else None
+
+
 def to_python_re(regex: str, names: Sequence[str], paper_dialect: bool = False) -> str:
     """Map each label to one private-use character; Python's own ``re``
     parser then parses the expression (no parser of ours is involved)."""
-    out = []
-    for kind, v in tokenize(regex, names):
-        if kind == "lab":
-            out.append(chr(0xE000 + v))
-        elif v == "+" and paper_dialect:
-            out.append("|")
+    order, pat = _o2_label_pattern(names)
+    out, i = [], 0
+    while i < len(regex):
+        c = regex[i]
+        if c.isspace() or c in "./":
+            i += 1
+        elif c in "()|*?":
+            out.append(c)
+            i += 1
+        elif c == "+":
+            out.append("|" if paper_dialect else "+")
+            i += 1
         else:
-            out.append(v)
+            m = pat.match(regex, i) if pat else None
+            if not m:
+                raise OracleError(OG_ELABEL, i, regex)
+            out.append(chr(0xE000 + list(names).index(m.group(0))))
+            i = m.end()
     return "".join(out)
+
+
+def _o2_num_labels(regex: str, names: Sequence[str]) -> int:
+    """Label occurrences in rho (O2's walk-length bound)."""
+    return sum(1 for ch in to_python_re(regex, names) if ord(ch) >= 0xE000)
 
 
 def brute_force(graph, regex: str, paper_dialect: bool = False,
@@ -264,7 +288,7 @@ def brute_force(graph, regex: str, paper_dialect: bool = False,
     within it (pigeonhole on a shortest product path)."""
     pat = re.compile(to_python_re(regex, graph.label_names, paper_dialect))
     nv = graph.num_vertices
-    occ = sum(1 for k, _ in tokenize(regex, graph.label_names) if k == "lab")
+    occ = _o2_num_labels(regex, graph.label_names)
     if max_len is None:
         max_len = nv * (occ + 1)
     adj: Dict[int, List[Tuple[int, str]]] = {v: [] for v in range(nv)}

@@ -264,3 +264,26 @@ def test_uniform_generator_shape():
     g = synth.uniform_graph(2000, 20000, 4, seed=2)
     keys = set(zip(g.src.tolist(), g.label.tolist(), g.dst.tolist()))
     assert len(keys) == 20000 == g.num_edges
+
+
+def test_longest_match_label_vocabulary():
+    """Reading R3 pinned on a prefix-ambiguous vocabulary {reply, replyOf}:
+    O1 (C parser), O2 (its own scanner) and O3 all read 'replyOf*' as the
+    closure of the single label replyOf, and 'reply' as the other label.
+    Expected sets written out from Definition 1 on this 4-edge graph."""
+    names = ["reply", "replyOf"]
+    # 0 -replyOf-> 1 -replyOf-> 2 ; 0 -reply-> 3 ; 3 -replyOf-> 0
+    g = synth.Graph(4, np.array([0, 1, 0, 3], np.uint32), np.array([1, 2, 3, 0], np.uint32),
+                    np.array([1, 1, 0, 1], np.uint16), names).check()
+    ident = {(v, v) for v in range(4)}
+    want = {
+        "replyOf*": ident | {(0, 1), (0, 2), (1, 2), (3, 0), (3, 1), (3, 2)},
+        "reply": {(0, 3)},
+        "reply replyOf": {(0, 0)},
+        "reply.replyOf+": {(0, 0), (0, 1), (0, 2)},
+        "(replyOf|reply)+": {(a, b) for a in (0, 3) for b in range(4)} | {(0, 1), (0, 2), (1, 2)},
+    }
+    for rx, w in want.items():
+        assert oracle.pair_set(oracle.allpairs(g, rx)) == w, ("O1", rx)
+        assert oracle.brute_force(g, rx) == w, ("O2", rx)
+        assert oracle.algebra(g, rx) == w, ("O3", rx)
