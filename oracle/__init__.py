@@ -80,6 +80,10 @@ def _load():
     L.og_eval.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, u32p,
                           ctypes.c_uint64, ctypes.c_int, ctypes.c_int, u64p, u64p,
                           P(u32p), P(u32p), u64p]
+    L.og_eval_bounded.restype = ctypes.c_int
+    L.og_eval_bounded.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, u32p,
+                                  ctypes.c_uint64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, u64p, u64p,
+                                  P(u32p), P(u32p), u64p]
     L.og_free.argtypes = [ctypes.c_void_p]
     _lib = L
     return L
@@ -163,8 +167,10 @@ class Automaton:
 
 
 def eval_sources(og: OracleGraph, regex: str, sources=None, *, pairs: bool = True,
-                 use_dfa: bool = True, threads: int = 0, paper_dialect: bool = False):
+                 use_dfa: bool = True, threads: int = 0, paper_dialect: bool = False,
+                 max_hops: Optional[int] = None):
     """O1: single-source RPQ for each source (all of V when sources is None).
+    max_hops = k: only paths of length <= k (BFS depth bound).
 
     Returns dict(counts=u64[n], pe=u64[n], src=u32[], dst=u32[]) with pairs
     sorted by (source order given, target ascending)."""
@@ -180,9 +186,10 @@ def eval_sources(og: OracleGraph, regex: str, sources=None, *, pairs: bool = Tru
     pd = ctypes.POINTER(ctypes.c_uint32)()
     npairs = ctypes.c_uint64(0)
     threads = threads or os.cpu_count() or 1
-    st = L.og_eval(og.h, A.h, int(use_dfa), _ptr(sources, ctypes.c_uint32), n, threads,
-                   int(pairs), _ptr(counts, ctypes.c_uint64), _ptr(pe, ctypes.c_uint64),
-                   ctypes.byref(ps), ctypes.byref(pd), ctypes.byref(npairs))
+    st = L.og_eval_bounded(og.h, A.h, int(use_dfa), _ptr(sources, ctypes.c_uint32), n, threads,
+                           int(pairs), -1 if max_hops is None else int(max_hops),
+                           _ptr(counts, ctypes.c_uint64), _ptr(pe, ctypes.c_uint64),
+                           ctypes.byref(ps), ctypes.byref(pd), ctypes.byref(npairs))
     if st != 0:
         raise OracleError(st)
     out = {"counts": counts, "pe": pe, "sources": sources}
@@ -200,11 +207,11 @@ def eval_sources(og: OracleGraph, regex: str, sources=None, *, pairs: bool = Tru
 
 
 def allpairs(graph, regex: str, *, use_dfa: bool = True, threads: int = 0,
-             paper_dialect: bool = False, pairs: bool = True):
+             paper_dialect: bool = False, pairs: bool = True, max_hops: Optional[int] = None):
     """O1 all-pairs RPQ (x ranges over all of V, reading R11)."""
     og = OracleGraph(graph)
     return eval_sources(og, regex, None, pairs=pairs, use_dfa=use_dfa, threads=threads,
-                        paper_dialect=paper_dialect)
+                        paper_dialect=paper_dialect, max_hops=max_hops)
 
 
 def pair_set(res) -> set:

@@ -33,6 +33,12 @@
  *   R4  E is a SET of (u, label, w) triples (duplicates collapse).
  *   R5  self-loops are 1-hop paths.
  *
+ * Length bound (og_eval_bounded; "length constraints can be
+ * naturally enforced by controlling traversal depth"): the same BFS, but a
+ * product vertex first reached at depth d is expanded only if d < max_hops,
+ * so (x, y) is emitted iff some path of length <= max_hops has a word in
+ * L(rho); PE then counts the out-edges of the expanded vertices only.
+ *
  * Parity pins: see tests/test_oracle.py (paper's worked example P:84, P:104,
  * P:236; brute-force Definition 1; relational algebra; closed forms).
  */
@@ -592,13 +598,14 @@ typedef struct {
     const og_graph *g; const og_automaton *A; int use_dfa;
     const uint32_t *sources; uint64_t nsrc;
     int want_pairs;
+    int64_t max_hops;           /* length bound: expand only nodes at depth < max_hops; -1 = none */
     uint64_t *counts, *pe;
     uint32_t **tlist;           /* per source sorted targets (want_pairs) */
     volatile uint64_t next;     /* dynamic chunking counter */
     int failed;
 } job;
 
-typedef struct { uint32_t v; int q; } pv;   /* product vertex (vertex, state) */
+typedef struct { uint32_t v; int q; int64_t d; } pv;   /* product vertex (vertex, state), BFS depth */
 
 static void *worker(void *arg) {
     job *J = (job *)arg;
@@ -618,29 +625,35 @@ static void *worker(void *arg) {
         for (uint64_t si = base; si < end; si++) {
             uint32_t x = J->sources[si];
             uint64_t qh = 0, qt = 0, nt = 0, pe = 0;
-#define VISIT(V, Q) do {                                                        \
+#define VISIT(V, Q, D) do {                                                     \
         uint64_t _b = (uint64_t)(V) * nq + (uint64_t)(Q);                        \
         if (!((vis[_b >> 6] >> (_b & 63)) & 1)) {                                \
             vis[_b >> 6] |= 1ull << (_b & 63);                                  \
             if (qt == qcap) { qcap *= 2; queue = (pv *)realloc(queue, qcap * sizeof(pv)); } \
-            queue[qt].v = (V); queue[qt].q = (Q); qt++;                          \
+            queue[qt].v = (V); queue[qt].q = (Q); queue[qt].d = (D); qt++;       \
         } } while (0)
             if (nq > 0) {
                 if (J->use_dfa) {
-                    VISIT(x, 0);
+                    VISIT(x, 0, 0);
                 } else {
                     const uint64_t *c = A->closure + (size_t)A->tstart * A->cw;
-                    for (int q = 0; q < A->tn; q++) if (bs_test(c, q)) VISIT(x, q);
+                    for (int q = 0; q < A->tn; q++) if (bs_test(c, q)) VISIT(x, q, 0);
                 }
             }
             while (qh < qt) {
                 pv cur = queue[qh++];
+                /* FIFO order = nondecreasing depth, so cur.d is the length of
+                 * a shortest path to (cur.v, cur.q); with a bound, nodes at
+                 * depth max_hops are reached (and may be final) but their
+                 * out-edges are not traversed */
+                const int expand = J->max_hops < 0 || cur.d < J->max_hops;
                 int final_ = J->use_dfa ? A->dfinal[cur.q] : (cur.q == A->taccept);
                 if (final_ && !((tgt[cur.v >> 6] >> (cur.v & 63)) & 1)) {
                     tgt[cur.v >> 6] |= 1ull << (cur.v & 63);
                     if (nt == tcap) { tcap *= 2; targets = (uint32_t *)realloc(targets, tcap * 4); }
                     targets[nt++] = cur.v;
                 }
+                if (!expand) continue;
                 if (J->use_dfa) {
                     for (int ai = 0; ai < A->nalpha; ai++) {
                         int d2 = A->dnext[(size_t)cur.q * A->nalpha + ai];
@@ -648,7 +661,7 @@ static void *worker(void *arg) {
                         uint32_t l = (uint32_t)A->alpha[ai];
                         uint64_t s = (uint64_t)l * g->nv + cur.v;
                         pe += g->off[s + 1] - g->off[s];          /* product edges traversed */
-                        for (uint64_t k = g->off[s]; k < g->off[s + 1]; k++) VISIT(g->adj[k], d2);
+                        for (uint64_t k = g->off[s]; k < g->off[s + 1]; k++) VISIT(g->adj[k], d2, cur.d + 1);
                     }
                 } else {
                     for (int k = A->tlab_off[cur.q]; k < A->tlab_off[cur.q + 1]; k++) {
@@ -657,7 +670,7 @@ static void *worker(void *arg) {
                         uint64_t s = (uint64_t)l * g->nv + cur.v;
                         pe += g->off[s + 1] - g->off[s];
                         for (uint64_t e = g->off[s]; e < g->off[s + 1]; e++)
-                            for (int q2 = 0; q2 < A->tn; q2++) if (bs_test(c, q2)) VISIT(g->adj[e], q2);
+                            for (int q2 = 0; q2 < A->tn; q2++) if (bs_test(c, q2)) VISIT(g->adj[e], q2, cur.d + 1);
                     }
                 }
             }
@@ -691,11 +704,12 @@ out:
  *   want_pairs: *psrc and *pdst receive malloc'ed arrays of all pairs, sorted by
  *   (source order as given, y ascending); free with og_free.
  */
-int og_eval(const og_graph *g, const og_automaton *A, int use_dfa,
-            const uint32_t *sources, uint64_t nsrc, int nthreads, int want_pairs,
-            uint64_t *counts, uint64_t *pe, uint32_t **psrc, uint32_t **pdst, uint64_t *npairs) {
+int og_eval_bounded(const og_graph *g, const og_automaton *A, int use_dfa,
+                    const uint32_t *sources, uint64_t nsrc, int nthreads, int want_pairs, int64_t max_hops,
+                    uint64_t *counts, uint64_t *pe, uint32_t **psrc, uint32_t **pdst, uint64_t *npairs) {
     for (uint64_t i = 0; i < nsrc; i++) if (sources[i] >= g->nv) return OG_EINVAL;
     job J; memset(&J, 0, sizeof(J));
+    J.max_hops = max_hops;
     J.g = g; J.A = A; J.use_dfa = use_dfa; J.sources = sources; J.nsrc = nsrc;
     J.want_pairs = want_pairs; J.counts = counts; J.pe = pe;
     if (want_pairs) J.tlist = (uint32_t **)calloc(nsrc ? nsrc : 1, sizeof(uint32_t *));
@@ -718,6 +732,13 @@ int og_eval(const og_graph *g, const og_automaton *A, int use_dfa,
         *psrc = S; *pdst = D; *npairs = tot;
     }
     return OG_OK;
+}
+
+/* og_eval_bounded with max_hops = -1: no length bound (Definition 1) */
+int og_eval(const og_graph *g, const og_automaton *A, int use_dfa,
+            const uint32_t *sources, uint64_t nsrc, int nthreads, int want_pairs,
+            uint64_t *counts, uint64_t *pe, uint32_t **psrc, uint32_t **pdst, uint64_t *npairs) {
+    return og_eval_bounded(g, A, use_dfa, sources, nsrc, nthreads, want_pairs, -1, counts, pe, psrc, pdst, npairs);
 }
 
 void og_free(void *p) { free(p); }

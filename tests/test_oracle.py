@@ -287,3 +287,37 @@ def test_longest_match_label_vocabulary():
         assert oracle.pair_set(oracle.allpairs(g, rx)) == w, ("O1", rx)
         assert oracle.brute_force(g, rx) == w, ("O2", rx)
         assert oracle.algebra(g, rx) == w, ("O3", rx)
+
+
+def test_length_bounded_vs_brute_force():
+    """Length-bounded RPQs: O1 with max_hops = k equals O2 with
+    walks of length <= k (Definition 1 restricted to |path| <= k), in both
+    automaton modes, on tiny random graphs; k >= O2's bound = unbounded."""
+    rng = np.random.default_rng(17)
+    for it in range(60):
+        g = synth.random_small(rng, max_v=5, max_e=9)
+        for rx in ["a*", "(a|b)*c", "a b* c", "c+", "(a|b)*c*", "a?b"]:
+            for k in range(0, 5):
+                want = oracle.brute_force(g, rx, max_len=k)
+                for dfa in (True, False):
+                    got = oracle.pair_set(oracle.allpairs(g, rx, use_dfa=dfa, max_hops=k))
+                    assert got == want, (it, rx, k, dfa)
+            big = oracle.allpairs(g, rx, max_hops=10_000)
+            full = oracle.allpairs(g, rx)
+            assert oracle.pair_set(big) == oracle.pair_set(full)
+            assert np.array_equal(big["pe"], full["pe"])
+
+
+def test_length_bounded_chain_closed_form():
+    """a* on the chain 0 -a-> 1 -a-> ... -a-> n-1 with bound k: source i
+    reaches i..min(i+k, n-1); the expanded product vertices are those at
+    depth < k, each with one out-edge except vertex n-1, so
+    PE(i) = |{v : i <= v <= min(i+k-1, n-2)}|."""
+    n = 40
+    g = synth.chain_graph(n - 1)              # n vertices, n - 1 edges
+    for k in [0, 1, 2, 5, 39, 50]:
+        r = oracle.allpairs(g, "a*", max_hops=k)
+        want_pairs = {(i, j) for i in range(n) for j in range(i, min(i + k, n - 1) + 1)}
+        assert oracle.pair_set(r) == want_pairs, k
+        want_pe = [max(0, min(i + k - 1, n - 2) - i + 1) for i in range(n)]
+        assert r["pe"].tolist() == want_pe, k
