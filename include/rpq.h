@@ -148,6 +148,11 @@ rpq_status rpq_nfa_reverse(const rpq_nfa *a, rpq_nfa **out);
                                  counters); in COUNT mode fused into the count pass */
 #define RPQ_SOURCE_PE 64u     /* with RPQ_PER_SOURCE: per-source PE (rpq_result_source_pe); the
                                  per-source list then holds every source with a non-zero count OR PE */
+#define RPQ_BOUNDED 128u      /* length-bounded RPQ: only paths of <= opts.max_hops edges (P:1574-1575,
+                                 "length constraints ... enforced by controlling traversal depth").  Exact
+                                 BFS levels: discoveries go to a separate per-level array (24 instead of 16
+                                 bytes per state word, so B shrinks by 1/3); dense engine only; PE counts the
+                                 out-edges of the product vertices at depth < max_hops (those expanded) */
 
 typedef struct {
     uint32_t mode;              /* OR of the RPQ_* mode bits above; 0 = RPQ_COUNT */
@@ -158,6 +163,8 @@ typedef struct {
     void *cuda_stream;          /* cudaStream_t; NULL = default stream */
     uint32_t chunk_words;       /* 0 = auto; else words per work item (1,2,4,8,16,32) */
     uint32_t reserved;
+    uint32_t max_hops;          /* with RPQ_BOUNDED: the length bound k >= 0 (0 = epsilon pairs only) */
+    uint32_t pad0;
 } rpq_eval_opts;
 
 /* All-pairs: x ranges over all of V (R11).  With shard_count > 1 the result

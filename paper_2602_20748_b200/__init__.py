@@ -32,7 +32,7 @@ RPQ_ENOMEM, RPQ_ECUDA, RPQ_ECAPACITY, RPQ_EUNSUPPORTED = -4, -5, -6, -7
 RPQ_SYNTAX_PAPER, RPQ_NO_MINIMIZE = 1, 2
 RPQ_MAX_STATES, RPQ_MAX_TRANSITIONS, RPQ_MAX_QUERY_LABELS = 64, 256, 32
 RPQ_COUNT, RPQ_PAIRS, RPQ_PER_SOURCE, RPQ_STATS, RPQ_TIME_KERNELS = 1, 2, 4, 8, 16
-RPQ_PE, RPQ_SOURCE_PE = 32, 64
+RPQ_PE, RPQ_SOURCE_PE, RPQ_BOUNDED = 32, 64, 128
 RPQ_GRAPH_IN_EDGES = 1
 RPQ_MAX_COLS = 16
 
@@ -65,7 +65,8 @@ class rpq_eval_opts(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_uint32), ("batch_sources", ctypes.c_uint32),
                 ("hbm_budget_bytes", ctypes.c_uint64), ("shard_index", ctypes.c_uint32),
                 ("shard_count", ctypes.c_uint32), ("cuda_stream", ctypes.c_void_p),
-                ("chunk_words", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+                ("chunk_words", ctypes.c_uint32), ("reserved", ctypes.c_uint32),
+                ("max_hops", ctypes.c_uint32), ("pad0", ctypes.c_uint32)]
 
 
 class rpq_plan_info(ctypes.Structure):
@@ -444,8 +445,12 @@ def rpq_compile_labels(label_names: Sequence[str], regex: str, flags: int = 0) -
 
 
 def make_opts(mode: int = RPQ_COUNT, batch_sources: int = 0, hbm_budget_bytes: int = 0, shard_index: int = 0,
-              shard_count: int = 1, stream=None, chunk_words: int = 0) -> rpq_eval_opts:
+              shard_count: int = 1, stream=None, chunk_words: int = 0, max_hops: Optional[int] = None) -> rpq_eval_opts:
+    """max_hops=k (not None) sets RPQ_BOUNDED: paths of length <= k only."""
     o = rpq_eval_opts()
+    if max_hops is not None:
+        mode |= RPQ_BOUNDED
+        o.max_hops = int(max_hops)
     o.mode, o.batch_sources, o.hbm_budget_bytes = mode, batch_sources, hbm_budget_bytes
     o.shard_index, o.shard_count, o.cuda_stream, o.chunk_words = shard_index, shard_count, stream, chunk_words
     return o

@@ -127,6 +127,14 @@ struct Ctrl {                  // per-level device counters / flags
 struct LevelArgs {
     uint64_t *Vis;             // visited: every reached bit, OR-ed in by red.or
     uint64_t *Done;            // bits already expanded (written only by the row's owner)
+    // The fused advance is  f = Front & ~Mark;  Mark |= f  (row owner), and
+    // discoveries are OR-ed into Disc.  Unbounded: Front = Disc = Vis,
+    // Mark = Done.  Length-bounded (RPQ_BOUNDED, exact BFS levels, reading
+    // D3): Front = N[par] (bits found by the previous level, zeroed when
+    // consumed), Mark = Vis (written only by row owners), Disc = N[par ^ 1].
+    uint64_t *Front, *Mark, *Disc;
+    uint32_t bounded;
+    uint32_t level_lim;        // last level (ctrl->levels) that may expand; ~0u = unbounded
     uint32_t *Xcur, *Xnext;    // chunk-activity bitmaps, one word per (row, xw)
     uint32_t *XBcur, *XBnext;  // block bitmaps: one bit per 32 X words
     uint64_t nxwords;          // rows * nxw
@@ -426,7 +434,7 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
                 for (int k = 0; k < KC; ++k) {
                     const uint64_t m = (e0 + e < cnt) ? (f[k] & ~b.vis[e][k]) : 0ull;
                     if (m) {
-                        red_or64(p.Vis + rb + ckk[k], m);
+                        red_or64(p.Disc + rb + ckk[k], m);
                         lm |= 1u << ((bits >> (8 * k)) & 0xffu);
                         if (STATS) st[S_N_RED]++;
                     }
@@ -499,6 +507,7 @@ template <bool STATS>
 __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, const Layout *__restrict__ Sg,
                                                                const LevelArgs p) {
     if (level_pull(p)) return;                 // bottom-up level: k_pull_prep + k_pull
+    if (*(volatile const uint32_t *)&p.ctrl->levels > p.level_lim) return;   // length bound reached
     __shared__ Layout S;
     __shared__ unsigned long long actS[ACT_SMEM_WORDS];
     load_layout(S, Sg, A.nq);
@@ -567,15 +576,16 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                     nk += has;
                     bits |= (uint64_t)bt << (8 * k);
                     const bool ok = has && lane_ok && xw * 32u * p.cw + bt * p.cw + lane < p.nw;
-                    f[k] = ok ? ld_cg(p.Vis + rb + bt * p.cw) : 0ull;
-                    dd[k] = ok ? p.Done[rb + bt * p.cw] : ~0ull;
+                    f[k] = ok ? ld_cg(p.Front + rb + bt * p.cw) : 0ull;
+                    dd[k] = ok ? p.Mark[rb + bt * p.cw] : ~0ull;
                 }
 #pragma unroll
                 for (int k = 0; k < KGRP; ++k) {
                     const uint32_t bt = (uint32_t)(bits >> (8 * k)) & 0xffu;
+                    if (p.bounded && f[k]) p.Front[rb + bt * p.cw] = 0ull;   // N[par] consumed
                     f[k] &= ~dd[k];
                     if (f[k]) {
-                        p.Done[rb + bt * p.cw] = dd[k] | f[k];
+                        p.Mark[rb + bt * p.cw] = dd[k] | f[k];
                         // sources of this frontier word may gain bits next level
                         if (p.pull_mode) act_or(actS, p.ActNext, (uint32_t)(rb - row * p.nw) + bt * p.cw, f[k]);
                         if (STATS) st[S_WORD_ITEMS]++;
@@ -656,6 +666,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
 template <bool STATS>
 __global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A, const Layout *__restrict__ Sg,
                                                                    const LevelArgs p) {
+    if (*(volatile const uint32_t *)&p.ctrl->levels > p.level_lim) return;   // length bound reached
     __shared__ Layout S;
     load_layout(S, Sg, A.nq);
     const int lane = threadIdx.x & 31;
@@ -983,7 +994,7 @@ __global__ void __launch_bounds__(256) k_seed_lanes(const DevAuto A, const Layou
             const uint64_t tbase = S.row_base[q2] - S.lo[q2];
             for (uint32_t j = beg; j < end; ++j) {
                 const uint64_t trow = tbase + __ldg(A.nbr[slot] + j);
-                red_or64(p.Vis + trow * p.nw + w, bit);
+                red_or64(p.Disc + trow * p.nw + w, bit);
                 if (live2) {
                     red_or32(p.Xnext + trow * p.nxw + (c >> 5), 1u << (c & 31u));
                     act = true;
@@ -1397,6 +1408,19 @@ __global__ void k_clear_dense(uint64_t *Vis, uint64_t *Done, uint64_t words, uin
     for (uint64_t i = i0; i < words; i += st) { Vis[i] = 0; Done[i] = 0; }
     for (uint64_t i = i0; i < nxwords; i += st) TX[i] = 0;
     for (uint64_t i = i0; i < ntu; i += st) TU[i] = 0;
+}
+
+// Length-bounded evaluation ends with the last level's discoveries (depth =
+// the bound) still in N: fold both N arrays into Vis and zero them.
+__global__ void k_merge_bounded(uint64_t *Vis, uint64_t *N0, uint64_t *N1, uint64_t words) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < words; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t a = N0[i], b = N1[i];
+        if (a | b) {
+            Vis[i] |= a | b;
+            N0[i] = 0;
+            N1[i] = 0;
+        }
+    }
 }
 
 __global__ void k_add_const(uint32_t *x, uint64_t n, uint32_t c) {
@@ -1882,6 +1906,10 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     // PE (product edges traversed, reading R12) from the post-pass only, no
     // in-kernel counters: fused into the COUNT pass (dense and touched paths)
     const bool want_pe = stats || (o.mode & RPQ_PE);
+    // length-bounded RPQ ("enforced by controlling traversal
+    // depth"): only paths of <= max_hops edges; exact BFS levels (reading D3)
+    const bool bounded = (o.mode & RPQ_BOUNDED) != 0;
+    const uint32_t max_hops = o.max_hops;
     const bool timeit = o.mode & RPQ_TIME_KERNELS;
     const uint32_t shard_count = o.shard_count ? o.shard_count : 1;
     if (o.shard_index >= shard_count) return rpq_fail(RPQ_EINVAL, "shard_index >= shard_count");
@@ -2031,7 +2059,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     // a final state without outgoing transitions collects result bits
     // without activity bitmaps, so its rows are not in the touched sets:
     // such automata clear and count densely
-    int dead_final = 0;
+    int dead_final = bounded ? 1 : 0;   // (bounded: the last level's bits are in no touched set)
     for (uint32_t q = 0; q < a->nq; ++q)
         if (((a->final_mask >> q) & 1ull) && a->off[q + 1] == a->off[q]) dead_final = 1;
 
@@ -2066,7 +2094,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         // PER_SOURCE / PAIRS the per-(source, 1024-vertex tile) counts; the
         // materialised pairs are allocated outside the budget, so those modes
         // keep half of it free
-        double per_word = 16.0 * R_max + 0.5 * R_max + 64.0 * 8 * 2;
+        double per_word = (bounded ? 24.0 : 16.0) * R_max + 0.5 * R_max + 64.0 * 8 * 2;
         uint64_t bud = budget;
         if (want_ps) {
             uint64_t hullv = 0;
@@ -2159,7 +2187,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     RPQ_CUDA_TRY(cudaMemsetAsync(d_stats, 0, NSTAT * 8 + 8, s));
     {
         const char *eng = getenv("RPQ_ENGINE");
-        const bool force_dense = (o.reserved & 1u) || (eng && !strcmp(eng, "dense"));
+        const bool force_dense = (o.reserved & 1u) || bounded || (eng && !strcmp(eng, "dense"));
         const bool force_sparse = eng && !strcmp(eng, "sparse");
         if (np && !force_dense) {
             unsigned long long *sc = (unsigned long long *)ws.get(np * 8);
@@ -2413,9 +2441,15 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     if (!h_cnt) RPQ_CUDA_TRY(cudaMallocHost(&h_cnt, 64));
     HubRec *hrecs = nullptr;
     HubItem *hitems = nullptr;
+    uint64_t *N1 = nullptr;
     if (nbatches && !sparse_done) {
         Vis = (uint64_t *)ws.get(words * 8);
-        Done = (uint64_t *)ws.get(words * 8);
+        Done = (uint64_t *)ws.get(words * 8);     // bounded: N0
+        if (bounded) {
+            N1 = (uint64_t *)ws.get(words * 8);
+            if (!N1) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (bounded state)"));
+            RPQ_CUDA_TRY(cudaMemsetAsync(N1, 0, words * 8, s));
+        }
         X0 = (uint32_t *)ws.get(nxwords * 4 + 128);
         X1 = (uint32_t *)ws.get(nxwords * 4 + 128);
         XB0 = (uint32_t *)ws.get(xbwords * 4);
@@ -2480,7 +2514,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     uint64_t *Act = nullptr;
     {
         uint32_t mode = pull_avail ? 1u : 0u;
-        if (CW != 32 || !nbatches || sparse_done) mode = 0;
+        if (CW != 32 || !nbatches || sparse_done || bounded) mode = 0;
         if (mode) {
             Act = (uint64_t *)ws.get(nw * 16);
             if (!Act) mode = 0;
@@ -2490,11 +2524,18 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         P0.ActCur = Act;
         P0.ActNext = Act ? Act + nw : nullptr;
     }
+    P0.bounded = bounded ? 1u : 0u;
+    // levels (ctrl->levels, counted from 1) that may expand: level L performs
+    // hop L, or hop L + 1 when the seeds were expanded by k_seed_expand
+    P0.level_lim = !bounded ? ~0u : skip_q0 ? (max_hops ? max_hops - 1 : 0) : max_hops;
+    if (bounded) { P0.Front = Done; P0.Mark = Vis; P0.Disc = N1; }   // N0 = the Done array
+    else { P0.Front = Vis; P0.Mark = Done; P0.Disc = Vis; }
     P1 = P0;
     P1.par = 1;
     std::swap(P1.Xcur, P1.Xnext);
     std::swap(P1.XBcur, P1.XBnext);
     std::swap(P1.ActCur, P1.ActNext);
+    if (bounded) std::swap(P1.Front, P1.Disc);
     const int lgrid = 148 * RPQ_LEVEL_MINB;   // persistent: warps fetch work units dynamically
     const int hgrid = 148 * RPQ_HUB_MINB;
     // The instantiated level graph is cached per thread and reused when every
@@ -2631,10 +2672,11 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         RPQ_CUDA_TRY(cudaMemcpyAsync(d_layout, d_layouts + lay_i, sizeof(Layout), cudaMemcpyDeviceToDevice, s));
         ++lay_i;
         if (Act) RPQ_CUDA_TRY(cudaMemsetAsync(Act, 0, nw * 16, s));
-        k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, Vis, X0, XB0, (uint32_t)nw, (uint32_t)nxw, CW, ctrl,
-                                            skip_q0 ? 1 : 0, Act);
+        // seeds: into Vis, or (bounded) into N0, the first level's frontier
+        k_seed<<<grid_for(nb), 256, 0, s>>>(S, cand, pidx, b0, nb, bounded ? Done : Vis, X0, XB0, (uint32_t)nw,
+                                            (uint32_t)nxw, CW, ctrl, skip_q0 ? 1 : 0, Act);
         ST.kernel_launches++;
-        if (skip_q0) {
+        if (skip_q0 && (!bounded || max_hops >= 1)) {
             const int sg = grid_for((uint64_t)nb * 32, 256, 148 * 8);
             const int seed_lanes = getenv("RPQ_SEED_WARPS") ? 0 : 1;
             if (seed_lanes) k_seed_lanes<<<grid_for(nb), 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
@@ -2664,19 +2706,36 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         PT.mark("levels");
         HM("levels enqueued");
         if (st != RPQ_OK) return fail(st);
+        // bounded: the loop may have stopped with activity left (levels past
+        // the bound return at once): clear the bitmaps for the next batch
+        if (bounded) {
+            RPQ_CUDA_TRY(cudaMemsetAsync(X0, 0, nxwords * 4 + 128, s));
+            RPQ_CUDA_TRY(cudaMemsetAsync(X1, 0, nxwords * 4 + 128, s));
+            RPQ_CUDA_TRY(cudaMemsetAsync(XB0, 0, xbwords * 4, s));
+            RPQ_CUDA_TRY(cudaMemsetAsync(XB1, 0, xbwords * 4, s));
+        }
+        // (bounded: Vis holds exactly the expanded bits (depth < bound) until
+        // k_merge_bounded below adds the last level's; PE is taken before)
         if (want_spe) {   // per-source PE of this batch -> cand_pe
             unsigned long long *bpe = (unsigned long long *)ws.get((uint64_t)nb * 8);
             if (!bpe) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
             RPQ_CUDA_TRY(cudaMemsetAsync(bpe, 0, (uint64_t)nb * 8, s));
             k_source_pe<<<148 * 8, 256, 0, s>>>(A, S, Vis, (uint32_t)nw, nb, bpe);
-            if (skip_q0) k_source_pe_seeds<<<grid_for(nb), 256, 0, s>>>(A, cand, pidx, b0, nb, bpe);
+            if (skip_q0 && (!bounded || max_hops >= 1))
+                k_source_pe_seeds<<<grid_for(nb), 256, 0, s>>>(A, cand, pidx, b0, nb, bpe);
             k_scatter_counts<<<grid_for(nb), 256, 0, s>>>(bpe, pidx, b0, nb, cand_pe);
             ST.kernel_launches += skip_q0 ? 3 : 2;
         }
         if (want_pe) {   // PE after the fact (exact for push and pull levels alike)
-            if (want_ps) k_pe_rows<<<148 * 8, 256, 0, s>>>(A, S, Vis, (uint32_t)nw, d_stats + S_PE_POST);
-            if (skip_q0) k_pe_seeds<<<grid_for(nb), 256, 0, s>>>(A, cand, pidx, b0, nb, d_stats + S_PE_POST);
-            ST.kernel_launches += (want_ps ? 1 : 0) + (skip_q0 ? 1 : 0);
+            const bool rows = want_ps || bounded;   // else fused into the count pass
+            const bool seeds = skip_q0 && (!bounded || max_hops >= 1);
+            if (rows) k_pe_rows<<<148 * 8, 256, 0, s>>>(A, S, Vis, (uint32_t)nw, d_stats + S_PE_POST);
+            if (seeds) k_pe_seeds<<<grid_for(nb), 256, 0, s>>>(A, cand, pidx, b0, nb, d_stats + S_PE_POST);
+            ST.kernel_launches += (rows ? 1 : 0) + (seeds ? 1 : 0);
+        }
+        if (bounded) {
+            k_merge_bounded<<<148 * 8, 256, 0, s>>>(Vis, Done, N1, words);
+            ST.kernel_launches++;
         }
         // X and XB are all zero again here (the last level activated
         // nothing).  Extraction reads Vis of the final states.
@@ -2688,9 +2747,10 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             // there from the touched-unit count); no host round trip.  With
             // PE the count pass reads every state's rows (hull of all ranges).
             const Range all_hull = lay_all[lay_i - 1];
-            const uint32_t clo = want_pe ? (all_hull.empty() ? 0 : all_hull.lo) : vlo;
-            const uint64_t cn = want_pe ? (all_hull.empty() ? 0 : (uint64_t)all_hull.hi - all_hull.lo + 1) : vn;
-            unsigned long long *pe_out = want_pe ? d_stats + S_PE_POST : nullptr;
+            const bool fuse_pe = want_pe && !bounded;
+            const uint32_t clo = fuse_pe ? (all_hull.empty() ? 0 : all_hull.lo) : vlo;
+            const uint64_t cn = fuse_pe ? (all_hull.empty() ? 0 : (uint64_t)all_hull.hi - all_hull.lo + 1) : vn;
+            unsigned long long *pe_out = (want_pe && !bounded) ? d_stats + S_PE_POST : nullptr;
             k_count_touched<<<148 * 8, 256, 0, s>>>(A, S, P0, nunits, d_total, dead_final, pe_out);
             if (cn) k_count_total<<<grid_for(cn * 32), 256, 0, s>>>(A, S, Vis, clo, cn, (uint32_t)nw, d_total, ctrl,
                                                                      nunits, dead_final, pe_out);
