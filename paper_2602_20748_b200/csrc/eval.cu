@@ -2003,24 +2003,55 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     }
 
     // ---- candidate sources and the productive subset P --------------------
+    // all-pairs: the candidates 0..|V|-1 and the productive set come from
+    // the graph's plan cache (no device round trip after the first query)
+    const bool allpairs = d_cand_in == nullptr;
     const uint32_t *cand = d_cand_in;
+    std::unique_lock<std::mutex> plan_lk(g->plan_mu, std::defer_lock);
     if (!cand) {
         nsrc = g->nv;
-        uint32_t *iota = (uint32_t *)ws.get(nsrc * 4);
-        if (!iota) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
-        k_iota<<<grid_for(nsrc), 256, 0, s>>>(iota, nsrc);
-        ST.kernel_launches++;
-        cand = iota;
+        plan_lk.lock();
+        if (!g->d_iota) {
+            uint32_t *iota = (uint32_t *)graph_alloc(g, nsrc * 4, s);
+            if (!iota) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
+            k_iota<<<grid_for(nsrc), 256, 0, s>>>(iota, nsrc);
+            ST.kernel_launches++;
+            g->d_iota = iota;
+        }
+        cand = g->d_iota;
+        plan_lk.unlock();
     }
+    // q0's labels (plan-cache key of the productive set)
+    std::vector<uint32_t> q0_labels;
+    for (uint32_t t = a->nq ? a->off[0] : 0; a->nq && t < a->off[1]; ++t) q0_labels.push_back(a->label[t]);
+    std::sort(q0_labels.begin(), q0_labels.end());
+    q0_labels.erase(std::unique(q0_labels.begin(), q0_labels.end()), q0_labels.end());
     uint8_t *flag = (uint8_t *)ws.get(std::max<uint64_t>(nsrc, 1));
-    uint32_t *pidx = (uint32_t *)ws.get(std::max<uint64_t>(nsrc, 1) * 4);
+    uint32_t *pidx = nullptr;
+    const std::vector<uint32_t> *h_pidx = nullptr;   // host copy (all-pairs, cached)
     uint64_t *d_np = (uint64_t *)ws.get(32);
-    if (!flag || !pidx || !d_np) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
+    if (!flag || !d_np) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
     uint64_t np = 0;
     uint32_t p_first_d = 0, p_last_d = 0;
     if (nsrc && a->nq) {
         k_productive<<<grid_for(nsrc), 256, 0, s>>>(A, cand, nsrc, flag);
         ST.kernel_launches++;
+    }
+    if (allpairs && nsrc && a->nq) {
+        std::lock_guard<std::mutex> lk(g->plan_mu);
+        for (auto *e : g->prod_cache)
+            if (e->reverse == (reverse ? 1u : 0u) && e->labels == q0_labels) {
+                pidx = e->d_pidx;
+                h_pidx = &e->h_pidx;
+            }
+    }
+    if (h_pidx) {
+        np = h_pidx->size();
+        p_first_d = np ? (*h_pidx)[0] : 0;            // cand = iota: vertex id = index
+        p_last_d = np ? (*h_pidx)[np - 1] : 0;
+    } else if (nsrc && a->nq) {
+        pidx = (uint32_t *)ws.get(std::max<uint64_t>(nsrc, 1) * 4);
+        if (!pidx) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
         size_t tb = 0;
         thrust::counting_iterator<uint32_t> it(0);
         cub::DeviceSelect::Flagged(nullptr, tb, it, flag, pidx, d_np, (int64_t)nsrc, s);
@@ -2036,8 +2067,31 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         p_first_d = (uint32_t)hb3[1];
         p_last_d = (uint32_t)hb3[2];
         HM("np readback");
+        if (allpairs) {   // remember the productive set for the next query on this graph
+            auto *e = new rpq_graph::ProdEntry();
+            e->reverse = reverse ? 1u : 0u;
+            e->labels = q0_labels;
+            e->h_pidx.resize(np);
+            e->d_pidx = (uint32_t *)graph_alloc(g, std::max<uint64_t>(np, 1) * 4, s);
+            if (!e->d_pidx) {
+                delete e;
+            } else {
+                if (np) {
+                    RPQ_CUDA_TRY(cudaMemcpyAsync(e->d_pidx, pidx, np * 4, cudaMemcpyDeviceToDevice, s));
+                    RPQ_CUDA_TRY(cudaMemcpyAsync(e->h_pidx.data(), pidx, np * 4, cudaMemcpyDeviceToHost, s));
+                    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                }
+                std::lock_guard<std::mutex> lk(g->plan_mu);
+                g->prod_cache.push_back(e);
+                h_pidx = &e->h_pidx;
+            }
+        }
     } else if (nsrc) {
         RPQ_CUDA_TRY(cudaMemsetAsync(flag, 0, nsrc, s));
+    }
+    if (!pidx) {
+        pidx = (uint32_t *)ws.get(std::max<uint64_t>(nsrc, 1) * 4);
+        if (!pidx) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sources)"));
     }
     ST.productive_sources = np;
     PT.mark("productive sources");
@@ -2144,7 +2198,12 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     // batch boundaries: first/last productive candidate index of each batch
     // and their vertex ids (one kernel + one copy for all batches)
     std::vector<uint32_t> bfirst(nbatches), blast(nbatches), sfirst(nbatches), slast(nbatches);
-    if (nbatches) {
+    if (nbatches && h_pidx) {   // all-pairs: candidate index = vertex id
+        for (uint64_t b = 0; b < nbatches; ++b) {
+            bfirst[b] = sfirst[b] = (*h_pidx)[b * B];
+            blast[b] = slast[b] = (*h_pidx)[std::min<uint64_t>(np, (b + 1) * B) - 1];
+        }
+    } else if (nbatches) {
         uint32_t *d_bounds = (uint32_t *)ws.get(nbatches * 16);
         if (!d_bounds) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
         k_batch_bounds<<<grid_for(nbatches), 256, 0, s>>>(pidx, cand, np, B, nbatches, d_bounds);
@@ -2198,7 +2257,23 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             if (!sc || !sov || !tov || !tlist || !d_nt)
                 return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (sparse)"));
             bool use = force_sparse;
-            if (!use) {
+            // all-pairs: the engine decision is a property of (graph,
+            // automaton) -- cached in the graph after the first sample
+            std::vector<uint32_t> sig;
+            int cached = -1;
+            if (allpairs && !use) {
+                sig = {reverse ? 1u : 0u, a->nq, (uint32_t)a->final_mask, (uint32_t)(a->final_mask >> 32)};
+                for (size_t t = 0; t < a->from.size(); ++t) {
+                    sig.push_back(a->from[t]);
+                    sig.push_back(a->label[t]);
+                    sig.push_back(a->to[t]);
+                }
+                std::lock_guard<std::mutex> lk(g->plan_mu);
+                for (auto &e : g->engine_cache)
+                    if (e.first == sig) cached = e.second;
+            }
+            if (cached >= 0) use = cached != 0;
+            if (!use && cached < 0) {
                 const uint64_t ns = std::min<uint64_t>(np, 2048);
                 uint32_t *didx = (uint32_t *)ws.get(ns * 4);
                 if (!didx) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
@@ -2215,6 +2290,10 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                 RPQ_CUDA_TRY(cudaStreamSynchronize(s));
                 HM("sparse sample");
                 use = nov * 50 <= ns;   // <= 2 % of the sample overflows
+                if (allpairs) {
+                    std::lock_guard<std::mutex> lk(g->plan_mu);
+                    g->engine_cache.emplace_back(sig, use ? 1 : 0);
+                }
             }
             if (use) {
                 // full pass over this shard's productive sources
@@ -2811,18 +2890,19 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     }
 
     if (sparse_done) total = sparse_total;
-    if (!want_ps && nbatches && !sparse_done) {
-        unsigned long long t = 0;
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&t, d_total, 8, cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-        total += t;
-    }
-    for (auto &e : tev) {
-        float ms = 0;
-        cudaEventSynchronize(e.second);
-        cudaEventElapsedTime(&ms, e.first, e.second);
-        ST.expand_ms += ms;
-    }
+    // everything the host still needs (device COUNT total, |listed sources|,
+    // level counter, statistics) comes back in ONE synchronisation at the end
+    struct Fin {
+        unsigned long long total;
+        uint64_t n_ps;
+        Ctrl ctrl;
+        unsigned long long hs[NSTAT];
+    };
+    static thread_local Fin *fin = nullptr;
+    if (!fin) RPQ_CUDA_TRY(cudaMallocHost(&fin, sizeof(Fin)));
+    memset(fin, 0, sizeof(Fin));
+    const bool dev_total = !want_ps && nbatches && !sparse_done;
+    if (dev_total) RPQ_CUDA_TRY(cudaMemcpyAsync(&fin->total, d_total, 8, cudaMemcpyDeviceToHost, s));
     PT.mark("extraction");
     HM("extraction+readback");
     // ---- result assembly ---------------------------------------------------
@@ -2880,21 +2960,31 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         if (want_spe)
             cub::DeviceSelect::Flagged(tmp, tb1, cand_pe, nz, (unsigned long long *)res->ps_pe, d_n, (int64_t)nsrc, s);
         cub::DeviceSelect::Flagged(tmp, tb2, cand, nz, res->ps_src, d_n, (int64_t)nsrc, s);
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&res->n_ps, d_n, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&fin->n_ps, d_n, 8, cudaMemcpyDeviceToHost, s));
+    }
+    if (nbatches && !sparse_done) RPQ_CUDA_TRY(cudaMemcpyAsync(&fin->ctrl, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
+    if (stats || want_pe) RPQ_CUDA_TRY(cudaMemcpyAsync(fin->hs, d_stats, sizeof(fin->hs), cudaMemcpyDeviceToHost, s));
+    cudaEventRecord(e_end, s);
+    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    if (dev_total) {
+        total += fin->total;
+        res->count = total;
+    }
+    if (want_ps && nsrc) res->n_ps = fin->n_ps;
+    for (auto &e : tev) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e.first, e.second);
+        ST.expand_ms += ms;
     }
     if (nbatches && !sparse_done) {
-        Ctrl hc{};
-        RPQ_CUDA_TRY(cudaMemcpyAsync(&hc, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        const Ctrl &hc = fin->ctrl;
         ST.levels = hc.levels;
         if (LG.exec)
             ST.kernel_launches += (2ull + (need_hub ? 1 : 0) + (P0.pull_mode ? 2 : 0)) * hc.levels + (hc.levels + 1) / 2;
         ST.expand_launches = 2ull * ST.levels;
     }
     if (stats || want_pe) {
-        unsigned long long hs[NSTAT];
-        RPQ_CUDA_TRY(cudaMemcpyAsync(hs, d_stats, sizeof(hs), cudaMemcpyDeviceToHost, s));
-        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        const unsigned long long *hs = fin->hs;
         // dense batches: PE after the fact (k_pe_rows/k_pe_seeds); the sparse
         // tiers count it per source (S_PE)
         ST.product_edges = hs[S_PE_POST] + (sparse_done ? hs[S_PE] : 0ull) + sub_pe;
@@ -2911,8 +3001,6 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         ST.activations = hs[S_X_RED];
         ST.next_reds = hs[S_N_RED];
     }
-    cudaEventRecord(e_end, s);
-    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
     float tms = 0;
     cudaEventElapsedTime(&tms, e_begin, e_end);
     ST.total_ms = tms;

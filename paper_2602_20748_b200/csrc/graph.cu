@@ -99,14 +99,14 @@ struct Cleanup {
 // Long-lived graph blocks: the caller's allocator when one was installed at
 // load time (rpq_set_allocator), else plain cudaMalloc (not the stream pool:
 // the graph outlives every stream the caller may use).
-static void *graph_alloc(const rpq_graph *g, size_t bytes, cudaStream_t s) {
+void *graph_alloc(const rpq_graph *g, size_t bytes, void *s) {
     if (g->alloc_snap && g->alloc_snap->alloc) return g->alloc_snap->alloc(bytes, (void *)s, g->alloc_snap->ctx);
     void *p = nullptr;
     if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
     return p;
 }
 
-static void graph_block_free(const rpq_graph *g, void *p) {
+void graph_block_free(const rpq_graph *g, void *p) {
     if (!p) return;
     if (g->alloc_snap && g->alloc_snap->free_) g->alloc_snap->free_(p, nullptr, g->alloc_snap->ctx);
     else cudaFree(p);
@@ -121,6 +121,11 @@ extern "C" void rpq_graph_free(rpq_graph *g) {
         graph_block_free(g, g->nbr_base[p]);
     }
     graph_block_free(g, g->vlabel);
+    graph_block_free(g, g->d_iota);
+    for (auto *e : g->prod_cache) {
+        graph_block_free(g, e->d_pidx);
+        delete e;
+    }
     delete g->alloc_snap;
     delete g;
     dev_available_invalidate();

@@ -43,7 +43,25 @@ struct rpq_graph {
     // allocator the CSR blocks came from (rpq_set_allocator at load time;
     // null functions = cudaMalloc / cudaFree)
     struct AllocSnap *alloc_snap = nullptr;
+    // Per-graph query-plan cache (the graph is immutable, so these depend
+    // only on the automaton): all-pairs candidates 0..nv-1, the productive
+    // sources of each set of labels leaving q0 (device + host copies), and
+    // the sparse/dense engine decision per automaton.  Filled by the first
+    // all-pairs query that needs them; freed with the graph.
+    struct ProdEntry {
+        uint32_t reverse;
+        std::vector<uint32_t> labels;    // sorted labels of q0's transitions
+        uint32_t *d_pidx = nullptr;      // productive candidate indices (graph-owned)
+        std::vector<uint32_t> h_pidx;
+    };
+    mutable std::mutex plan_mu;
+    mutable uint32_t *d_iota = nullptr;  // [nv] 0, 1, ..., nv - 1
+    mutable std::vector<ProdEntry *> prod_cache;
+    mutable std::vector<std::pair<std::vector<uint32_t>, int>> engine_cache;   // automaton signature -> sparse?
 };
+// graph-owned device blocks (rpq_set_allocator at load time, else cudaMalloc)
+void *graph_alloc(const rpq_graph *g, size_t bytes, void *stream);
+void graph_block_free(const rpq_graph *g, void *p);
 
 // ---- automaton ("automata plan") ------------------------------
 struct rpq_nfa {

@@ -26,7 +26,7 @@ def _free_port():
     return p
 
 
-GRAPH = dict(num_vertices=20000, num_edges=80000, num_labels=3, seed=41)
+GRAPH = dict(num_vertices=8000, num_edges=32000, num_labels=3, seed=41)
 
 
 def _worker(rank, world, port, rx, out_q):
