@@ -148,6 +148,10 @@ rpq_status rpq_nfa_reverse(const rpq_nfa *a, rpq_nfa **out);
                                  counters); in COUNT mode fused into the count pass */
 #define RPQ_SOURCE_PE 64u     /* with RPQ_PER_SOURCE: per-source PE (rpq_result_source_pe); the
                                  per-source list then holds every source with a non-zero count OR PE */
+#define RPQ_WCOJ 256u         /* crpq_eval: worst-case-optimal (generic) join instead of binary joins
+                                 (the WCOJ-based CQ method): variables are bound one at a time and
+                                 each new variable's candidates are the intersection of the sorted value
+                                 lists of every atom into it; same tuples, sorted the same way */
 #define RPQ_BOUNDED 128u      /* length-bounded RPQ: only paths of <= opts.max_hops edges (P:1574-1575,
                                  "length constraints ... enforced by controlling traversal depth").  Exact
                                  BFS levels: discoveries go to a separate per-level array (24 instead of 16

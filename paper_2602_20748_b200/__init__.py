@@ -32,7 +32,7 @@ RPQ_ENOMEM, RPQ_ECUDA, RPQ_ECAPACITY, RPQ_EUNSUPPORTED = -4, -5, -6, -7
 RPQ_SYNTAX_PAPER, RPQ_NO_MINIMIZE = 1, 2
 RPQ_MAX_STATES, RPQ_MAX_TRANSITIONS, RPQ_MAX_QUERY_LABELS = 64, 256, 32
 RPQ_COUNT, RPQ_PAIRS, RPQ_PER_SOURCE, RPQ_STATS, RPQ_TIME_KERNELS = 1, 2, 4, 8, 16
-RPQ_PE, RPQ_SOURCE_PE, RPQ_BOUNDED = 32, 64, 128
+RPQ_PE, RPQ_SOURCE_PE, RPQ_BOUNDED, RPQ_WCOJ = 32, 64, 128, 256
 RPQ_GRAPH_IN_EDGES = 1
 RPQ_MAX_COLS = 16
 

@@ -130,6 +130,90 @@ __global__ void k_iota32(uint32_t *x, uint64_t n) {
         x[i] = (uint32_t)i;
 }
 
+// ---- worst-case-optimal join (generic join, RPQ_WCOJ) --------------------
+// One extension step of the variable-at-a-time join ("the WCOJ-based
+// CQ method"; generic join / leapfrog intersection): every row of the table
+// binds a prefix of the matching order; the candidates of the next variable
+// are the INTERSECTION of the value lists of all atom indexes whose key end
+// is already bound (index = the atom relation sorted by (key, value)), minus
+// vertices failing the variable's label / constant, its self atoms (x -> x)
+// and its distinct-vertex filters.  A warp per row: the smallest
+// list is scanned by the lanes, every element binary-searched in the others.
+constexpr int WJ_MAXC = 8;
+struct ExtStep {
+    int nc;                                    // constraining indexes
+    const uint32_t *key[WJ_MAXC], *val[WJ_MAXC];
+    uint64_t n[WJ_MAXC];
+    int keycol[WJ_MAXC];                       // table column holding the index key
+    int nd;                                    // distinct filters against bound columns
+    int dcol[WJ_MAXC];
+    VarPred pred;
+    const uint8_t *selfok;                     // [nv] self atoms of the variable, or null
+};
+
+__device__ __forceinline__ bool in_sorted(const uint32_t *a, uint64_t lo, uint64_t hi, uint32_t x) {
+    const uint64_t end = hi;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo < end && a[lo] == x;
+}
+
+// WRITE = false: cnt[row] = number of extensions; true: write them at off[row]
+template <bool WRITE>
+__global__ void k_wcoj_extend(const ExtStep st, const uint32_t *const *tcols, uint32_t ncols, uint64_t nrows,
+                              unsigned long long *cnt, const unsigned long long *off, uint32_t *const *ocols) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (uint64_t r = wid; r < nrows; r += nwarps) {
+        uint64_t lo[WJ_MAXC], hi[WJ_MAXC];
+        int best = 0;
+        for (int c = 0; c < st.nc; ++c) {   // equal range of the row's key in index c
+            const uint32_t k = tcols[st.keycol[c]][r];
+            lo[c] = lower_bound_u32(st.key[c], st.n[c], k);
+            hi[c] = k == 0xffffffffu ? st.n[c] : lower_bound_u32(st.key[c], st.n[c], k + 1);
+            if (hi[c] - lo[c] < hi[best] - lo[best]) best = c;
+        }
+        unsigned long long o = WRITE ? off[r] : 0ull, found = 0;
+        for (uint64_t b0 = lo[best]; b0 < hi[best]; b0 += 32) {
+            const uint64_t i = b0 + lane;
+            bool ok = i < hi[best];
+            uint32_t e = ok ? st.val[best][i] : 0u;
+            ok = ok && st.pred.ok(e) && (!st.selfok || st.selfok[e]);
+            for (int d = 0; d < st.nd && ok; ++d) ok = e != tcols[st.dcol[d]][r];
+            for (int c = 0; c < st.nc && ok; ++c)
+                if (c != best) ok = in_sorted(st.val[c], lo[c], hi[c], e);
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (WRITE && ok) {
+                const unsigned long long p = o + found + __popc(m & lt);
+                for (uint32_t j = 0; j < ncols; ++j) ocols[j][p] = tcols[j][r];
+                ocols[ncols][p] = e;
+            }
+            found += __popc(m);
+        }
+        if (!WRITE && lane == 0) cnt[r] = found;
+    }
+}
+
+__global__ void k_mark_keys(const uint32_t *key, uint64_t n, uint8_t *mark) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        mark[key[i]] = 1;
+}
+
+__global__ void k_and_flags(uint8_t *a, const uint8_t *b, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        a[i] = a[i] && b[i];
+}
+
+// self atom x -rho-> x: mark v with (v, v) in the relation
+__global__ void k_mark_self(const uint32_t *s, const uint32_t *d, uint64_t n, uint8_t *mark) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        if (s[i] == d[i]) mark[s[i]] = 1;
+}
+
 // ---- host helpers ---------------------------------------------------------
 struct Pool {
     cudaStream_t s;
@@ -194,6 +278,227 @@ void add_stats(rpq_stats &a, const rpq_stats &b) {
     a.expand_ms += b.expand_ms;
 }
 
+// Generic join (RPQ_WCOJ): fills T with every variable bound (columns in the
+// matching order), distinct filters applied during the extension steps.
+rpq_status wcoj_join(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts &o, cudaStream_t s, Pool &P,
+                     rpq_stats &ST, const std::vector<int32_t> &vlab, const std::vector<int64_t> &vcst, Table &T) {
+    const uint32_t nvars = q->num_vars, natoms = q->num_atoms;
+    auto pred = [&](uint32_t v) { return VarPred{vcst[v], vlab[v], g->vlabel}; };
+    // ---- matching order: a constant (else the most-constrained variable)
+    // first, then repeatedly the variable with the most atoms into the bound
+    // set (ties: constant / label, then lowest id); disconnected -> R18
+    std::vector<int> pos(nvars, -1);
+    std::vector<uint32_t> ord;
+    for (uint32_t k = 0; k < nvars; ++k) {
+        int best = -1;
+        long bs = -1;
+        for (uint32_t v = 0; v < nvars; ++v) {
+            if (pos[v] >= 0) continue;
+            long links = 0, deg = 0;
+            for (uint32_t i = 0; i < natoms; ++i) {
+                const uint32_t x = q->atom_x[i], y = q->atom_y[i];
+                if (x != v && y != v) continue;
+                ++deg;
+                const uint32_t o2 = x == v ? y : x;
+                if (o2 != v && pos[o2] >= 0) ++links;
+            }
+            if (k > 0 && links == 0) continue;
+            const long sc = links * 10000 + (vcst[v] >= 0 ? 1000 : 0) + (vlab[v] >= 0 ? 100 : 0) + deg;
+            if (sc > bs) { bs = sc; best = (int)v; }
+        }
+        if (best < 0) return rpq_fail(RPQ_EUNSUPPORTED, "crpq_eval: disconnected pattern (R18)");
+        pos[best] = (int)k;
+        ord.push_back((uint32_t)best);
+    }
+    // ---- atom indexes, keyed by the end bound first ----
+    struct Index { uint32_t keyvar, valvar; uint32_t *key, *val; uint64_t n; };
+    std::vector<Index> idx;
+    std::vector<uint8_t *> selfok(nvars, nullptr);
+    const bool in_edges = g->in_csr.size() == g->csr.size();
+    for (uint32_t i = 0; i < natoms; ++i) {
+        const uint32_t x = q->atom_x[i], y = q->atom_y[i];
+        const bool self = x == y;
+        const bool fwd = self || pos[x] < pos[y];
+        const uint32_t kv = fwd ? x : y;           // key end = bound first
+        // traverse from the key end: forward from x, or the reversed
+        // automaton over the transposed graph from y (reverse plan);
+        // without in-edges, forward from all x and re-sort by (y, x)
+        const bool backward = !fwd && in_edges && !getenv("RPQ_CRPQ_FORWARD");
+        const uint32_t sv = fwd || backward ? kv : x;
+        rpq_nfa *rev = nullptr;
+        struct RevGuard { rpq_nfa **p; ~RevGuard() { delete *p; } } rg0{&rev};
+        if (backward) {
+            rpq_status rs = reverse_automaton(q->atom_nfa[i], &rev);
+            if (rs != RPQ_OK) return rs;
+        }
+        uint32_t *srcs = nullptr;
+        uint64_t nsrc = 0;
+        bool all_v = true;
+        if (vcst[sv] >= 0 || vlab[sv] >= 0) {   // candidates of the start variable
+            all_v = false;
+            uint8_t *flag = (uint8_t *)P.get(g->nv);
+            srcs = (uint32_t *)P.get((uint64_t)g->nv * 4);
+            uint64_t *d_n = (uint64_t *)P.get(8);
+            if (!flag || !srcs || !d_n) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            k_cand_flags<<<grid_for(g->nv), 256, 0, s>>>(pred(sv), g->nv, flag);
+            size_t tb = 0;
+            thrust::counting_iterator<uint32_t> it(0);
+            cub::DeviceSelect::Flagged(nullptr, tb, it, flag, srcs, d_n, (int64_t)g->nv, s);
+            void *tmp = P.get(tb);
+            if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            cub::DeviceSelect::Flagged(tmp, tb, it, flag, srcs, d_n, (int64_t)g->nv, s);
+            RPQ_CUDA_TRY(cudaMemcpyAsync(&nsrc, d_n, 8, cudaMemcpyDeviceToHost, s));
+            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        }
+        rpq_eval_opts ao = o;
+        ao.mode = RPQ_PAIRS | (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS));
+        ao.shard_index = 0;
+        ao.shard_count = 1;
+        if (backward) ao.reserved |= 2u;
+        rpq_result *rel = nullptr;
+        const rpq_nfa *enfa = backward ? rev : q->atom_nfa[i];
+        rpq_status st = all_v ? eval_sources_device(g, enfa, nullptr, 0, &ao, &rel)
+                              : eval_sources_device(g, enfa, srcs, nsrc, &ao, &rel);
+        if (st != RPQ_OK) return st;
+        add_stats(ST, rel->stats);
+        struct RelGuard { rpq_result *r; ~RelGuard() { rpq_result_release(r); } } rg{rel};
+        uint64_t n = rel->nrows;
+        // pool-owned (key, value) columns: forward and backward results are
+        // already sorted by (key, value); forward-evaluated backward indexes
+        // are re-sorted by (y, x)
+        std::vector<uint32_t *> rc(2);
+        for (int c = 0; c < 2; ++c) {
+            rc[c] = (uint32_t *)P.get(std::max<uint64_t>(n, 1) * 4);
+            if (!rc[c]) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            if (n) RPQ_CUDA_TRY(cudaMemcpyAsync(rc[c], rel->cols[c], n * 4, cudaMemcpyDeviceToDevice, s));
+        }
+        const uint32_t vv = self ? x : (fwd ? y : x);   // value end
+        if (!fwd && !backward && n) {
+            uint64_t *k1 = (uint64_t *)P.get(n * 8), *k2 = (uint64_t *)P.get(n * 8);
+            if (!k1 || !k2) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            k_pack_swap<<<grid_for(n), 256, 0, s>>>(rc[0], rc[1], n, k1);
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tb, k1, k2, (int64_t)n, 0, 64, s);
+            void *tmp = P.get(tb);
+            if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            cub::DeviceRadixSort::SortKeys(tmp, tb, k1, k2, (int64_t)n, 0, 64, s);
+            k_unpack<<<grid_for(n), 256, 0, s>>>(k2, n, rc[0], rc[1]);   // (y, x)
+        }
+        if (self) {   // x -rho-> x: a filter on x's candidates
+            if (!selfok[x]) {
+                selfok[x] = (uint8_t *)P.get(g->nv);
+                if (!selfok[x]) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+                RPQ_CUDA_TRY(cudaMemsetAsync(selfok[x], 1, g->nv, s));
+            }
+            uint8_t *m = (uint8_t *)P.get(g->nv);
+            if (!m) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            RPQ_CUDA_TRY(cudaMemsetAsync(m, 0, g->nv, s));
+            if (n) k_mark_self<<<grid_for(n), 256, 0, s>>>(rc[0], rc[1], n, m);
+            k_and_flags<<<grid_for(g->nv), 256, 0, s>>>(selfok[x], m, g->nv);
+            continue;
+        }
+        // drop pairs whose value fails its variable's label / constant
+        if (n) {
+            uint8_t *flag = (uint8_t *)P.get(n);
+            if (!flag) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            k_pair_flags<<<grid_for(n), 256, 0, s>>>(rc[0], rc[1], n, pred(vv), 0, flag, pred(kv), 1);
+            st = compact(P, rc, n, flag, s);
+            if (st != RPQ_OK) return st;
+        }
+        idx.push_back(Index{kv, vv, rc[0], rc[1], n});
+    }
+    // ---- first variable: its candidates that occur as a key of every index
+    const uint32_t v0 = ord[0];
+    {
+        uint8_t *flag = (uint8_t *)P.get(g->nv), *m = (uint8_t *)P.get(g->nv);
+        uint32_t *c0 = (uint32_t *)P.get((uint64_t)g->nv * 4);
+        uint64_t *d_n = (uint64_t *)P.get(8);
+        if (!flag || !m || !c0 || !d_n) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+        k_cand_flags<<<grid_for(g->nv), 256, 0, s>>>(pred(v0), g->nv, flag);
+        if (selfok[v0]) k_and_flags<<<grid_for(g->nv), 256, 0, s>>>(flag, selfok[v0], g->nv);
+        for (auto &ix : idx) {
+            if (ix.keyvar != v0) continue;
+            RPQ_CUDA_TRY(cudaMemsetAsync(m, 0, g->nv, s));
+            if (ix.n) k_mark_keys<<<grid_for(ix.n), 256, 0, s>>>(ix.key, ix.n, m);
+            k_and_flags<<<grid_for(g->nv), 256, 0, s>>>(flag, m, g->nv);
+        }
+        size_t tb = 0;
+        thrust::counting_iterator<uint32_t> it(0);
+        cub::DeviceSelect::Flagged(nullptr, tb, it, flag, c0, d_n, (int64_t)g->nv, s);
+        void *tmp = P.get(tb);
+        if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+        cub::DeviceSelect::Flagged(tmp, tb, it, flag, c0, d_n, (int64_t)g->nv, s);
+        uint64_t n0 = 0;
+        RPQ_CUDA_TRY(cudaMemcpyAsync(&n0, d_n, 8, cudaMemcpyDeviceToHost, s));
+        RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+        T.vars = {v0};
+        T.cols = {c0};
+        T.n = n0;
+    }
+    // ---- extension steps ----
+    for (uint32_t k = 1; k < nvars; ++k) {
+        const uint32_t v = ord[k];
+        ExtStep es{};
+        for (auto &ix : idx) {
+            if (ix.valvar != v || T.col_of(ix.keyvar) < 0) continue;
+            if (es.nc == WJ_MAXC) return rpq_fail(RPQ_EUNSUPPORTED, "crpq_eval: > %d atoms into one variable", WJ_MAXC);
+            es.key[es.nc] = ix.key;
+            es.val[es.nc] = ix.val;
+            es.n[es.nc] = ix.n;
+            es.keycol[es.nc] = T.col_of(ix.keyvar);
+            ++es.nc;
+        }
+        for (uint32_t d = 0; d < q->num_distinct; ++d) {
+            const uint32_t a = q->distinct_pairs[2 * d], b = q->distinct_pairs[2 * d + 1];
+            const uint32_t other = a == v ? b : (b == v ? a : UINT32_MAX);
+            if (other == UINT32_MAX) continue;
+            if (other == v) { T.n = 0; break; }            // distinct(v, v): nothing survives
+            const int c = T.col_of(other);
+            if (c < 0) continue;                            // filtered when `other` is bound
+            if (es.nd == WJ_MAXC) return rpq_fail(RPQ_EUNSUPPORTED, "crpq_eval: too many distinct filters");
+            es.dcol[es.nd++] = c;
+        }
+        es.pred = pred(v);
+        es.selfok = selfok[v];
+        uint32_t **d_in = (uint32_t **)P.get(T.cols.size() * sizeof(void *));
+        unsigned long long *cnt = (unsigned long long *)P.get(std::max<uint64_t>(T.n, 1) * 8);
+        unsigned long long *off = (unsigned long long *)P.get(std::max<uint64_t>(T.n, 1) * 8);
+        if (!d_in || !cnt || !off) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_in, T.cols.data(), T.cols.size() * sizeof(void *), cudaMemcpyHostToDevice, s));
+        uint64_t total = 0;
+        const int wg = grid_for(T.n * 32);
+        if (T.n) {
+            k_wcoj_extend<false><<<wg, 256, 0, s>>>(es, d_in, (uint32_t)T.cols.size(), T.n, cnt, nullptr, nullptr);
+            size_t tb = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, off, (int64_t)T.n, s);
+            void *tmp = P.get(tb);
+            if (!tmp) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, off, (int64_t)T.n, s);
+            unsigned long long a = 0, b = 0;
+            RPQ_CUDA_TRY(cudaMemcpyAsync(&a, off + T.n - 1, 8, cudaMemcpyDeviceToHost, s));
+            RPQ_CUDA_TRY(cudaMemcpyAsync(&b, cnt + T.n - 1, 8, cudaMemcpyDeviceToHost, s));
+            RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+            total = a + b;
+        }
+        std::vector<uint32_t *> nc(T.cols.size() + 1);
+        for (auto &c : nc) {
+            c = (uint32_t *)P.get(std::max<uint64_t>(total, 1) * 4);
+            if (!c) return rpq_fail(RPQ_ENOMEM, "crpq: out of device memory (%llu tuples)", (unsigned long long)total);
+        }
+        if (total) {
+            uint32_t **d_out = (uint32_t **)P.get(nc.size() * sizeof(void *));
+            if (!d_out) return rpq_fail(RPQ_ENOMEM, "crpq: oom");
+            RPQ_CUDA_TRY(cudaMemcpyAsync(d_out, nc.data(), nc.size() * sizeof(void *), cudaMemcpyHostToDevice, s));
+            k_wcoj_extend<true><<<wg, 256, 0, s>>>(es, d_in, (uint32_t)T.cols.size(), T.n, cnt, off, d_out);
+        }
+        for (auto c : T.cols) P.put(c);
+        T.cols = nc;
+        T.vars.push_back(v);
+        T.n = total;
+    }
+    return RPQ_OK;
+}
+
 }  // namespace
 
 extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts_in,
@@ -225,6 +530,10 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
         if (!q->distinct_pairs || q->distinct_pairs[2 * i] >= nvars || q->distinct_pairs[2 * i + 1] >= nvars)
             return rpq_fail(RPQ_EINVAL, "crpq_eval: bad distinct filter");
 
+    rpq_eval_opts o{};
+    if (opts_in) o = *opts_in;
+    const bool wcoj = (o.mode & RPQ_WCOJ) != 0;
+
     // ---- plan: constants first, then atoms sharing a bound variable -------
     std::vector<uint32_t> order;
     std::vector<int> done(natoms, 0), bound(nvars, 0);
@@ -252,8 +561,6 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
         order.push_back((uint32_t)best);
     }
 
-    rpq_eval_opts o{};
-    if (opts_in) o = *opts_in;
     RPQ_CUDA_TRY(cudaSetDevice(g->device));
     cudaStream_t s = (cudaStream_t)o.cuda_stream;
     Pool P{s, {}};
@@ -265,7 +572,11 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
     auto pred = [&](uint32_t v) { return VarPred{vcst[v], vlab[v], g->vlabel}; };
 
     Table T;
-    for (uint32_t k = 0; k < natoms; ++k) {
+    if (wcoj) {
+        rpq_status wst = wcoj_join(g, q, o, s, P, ST, vlab, vcst, T);
+        if (wst != RPQ_OK) return wst;
+    }
+    for (uint32_t k = 0; k < (wcoj ? 0u : natoms); ++k) {
         const uint32_t ai = order[k];
         const uint32_t x = q->atom_x[ai], y = q->atom_y[ai];
         const rpq_nfa *nfa = q->atom_nfa[ai];
