@@ -82,6 +82,16 @@ typedef struct {
 rpq_status rpq_graph_load(const rpq_graph_desc *desc, rpq_graph **out);
 void rpq_graph_free(rpq_graph *g);
 /* |V|, number of DISTINCT (u,l,w) triples, number of labels */
+/* Add an edge label whose edges are the given (src[i], dst[i]) pairs (device
+ * arrays if on_device, else host; duplicates collapse, reading R4), with its
+ * CSR (and in-edge CSR when the graph keeps in-edges).  The new label gets
+ * the next id (*label_id) and can be named in regexes compiled afterwards;
+ * automata compiled before stay valid (their vocabulary is a prefix).
+ * Used by the loop-cache plan (rpq_cache_closure).  Mutates g: not
+ * concurrently with evaluations on g.  EINVAL: bad argument, duplicate name,
+ * id >= |V|; EUNSUPPORTED: >= 2^32 pairs or 65535 labels. */
+rpq_status rpq_graph_add_label(rpq_graph *g, const char *name, const uint32_t *src, const uint32_t *dst,
+                               uint64_t n, int on_device, void *cuda_stream, uint32_t *label_id);
 rpq_status rpq_graph_info(const rpq_graph *g, uint32_t *num_vertices, uint64_t *num_edges,
                           uint32_t *num_labels);
 /* Device views (valid until rpq_graph_free) of label l's CSR. */
@@ -195,6 +205,23 @@ typedef struct {
     uint64_t state_words;
 } rpq_plan_info;
 rpq_status rpq_plan(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts, rpq_plan_info *info);
+
+/* Loop-cache plan (WavePlan A2): evaluate `inner` over all of
+ * V (PAIRS) and install R(inner) as the derived label `name`
+ * (rpq_graph_add_label).  A query a (b c)* d then runs as "a name? d" with
+ * inner = (b c)+: the closure is traversed once, not once per source batch.
+ * opts: stream / budget / RPQ_BOUNDED as for rpq_eval_allpairs.  Errors as
+ * rpq_eval_allpairs and rpq_graph_add_label. */
+rpq_status rpq_cache_closure(rpq_graph *g, const rpq_nfa *inner, const char *name, const rpq_eval_opts *opts,
+                             uint32_t *label_id);
+
+/* The loop-cache plan end to end: all-pairs R(prefix (loop)* suffix) as
+ * rpq_cache_closure((loop)+) into a fresh label L ("__loopN"), then
+ * rpq_eval_allpairs("(prefix) L? (suffix)") with opts.  prefix / suffix may
+ * be NULL or blank.  Same pairs as evaluating the regex directly (PE counts
+ * the rewritten query).  Adds a label to g (see rpq_graph_add_label). */
+rpq_status rpq_eval_loop_cached(rpq_graph *g, const char *prefix, const char *loop, const char *suffix,
+                                const rpq_eval_opts *opts, rpq_result **out);
 
 /* Single source x = src.  src >= |V| -> EINVAL. */
 rpq_status rpq_eval_single_source(const rpq_graph *g, const rpq_nfa *a, uint32_t src,

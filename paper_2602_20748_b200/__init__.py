@@ -127,6 +127,7 @@ EXPORTED = [
     "rpq_device_count", "rpq_version", "rpq_shard_plan", "rpq_trim_memory",
     "rpq_nfa_reverse", "rpq_eval_targets", "rpq_eval_single_target", "rpq_eval_allpairs_stream",
     "rpq_set_allocator", "rpq_plan", "rpq_result_batches", "rpq_result_source_pe",
+    "rpq_graph_add_label", "rpq_cache_closure", "rpq_eval_loop_cached",
 ]
 
 _c = {}
@@ -169,6 +170,11 @@ _c["rpq_result_stats"] = _proto("rpq_result_stats", _st, [_vp, _P(rpq_stats)])
 _c["rpq_result_free"] = _proto("rpq_result_free", None, [_vp])
 _c["rpq_result_batches"] = _proto("rpq_result_batches", _st, [_vp, _P(rpq_batch_info), ctypes.c_uint64, c_u64p])
 _c["rpq_plan"] = _proto("rpq_plan", _st, [_vp, _vp, _P(rpq_eval_opts), _P(rpq_plan_info)])
+_c["rpq_graph_add_label"] = _proto("rpq_graph_add_label", _st, [_vp, ctypes.c_char_p, _vp, _vp, ctypes.c_uint64,
+                                                                ctypes.c_int, _vp, c_u32p])
+_c["rpq_eval_loop_cached"] = _proto("rpq_eval_loop_cached", _st, [_vp, ctypes.c_char_p, ctypes.c_char_p,
+                                                                  ctypes.c_char_p, _P(rpq_eval_opts), _P(_vp)])
+_c["rpq_cache_closure"] = _proto("rpq_cache_closure", _st, [_vp, _vp, ctypes.c_char_p, _P(rpq_eval_opts), c_u32p])
 _c["rpq_result_source_pe"] = _proto("rpq_result_source_pe", _st, [_vp, c_u64p, ctypes.c_uint64, c_u64p])
 _c["rpq_last_error"] = _proto("rpq_last_error", ctypes.c_char_p, [])
 _c["rpq_device_count"] = _proto("rpq_device_count", _st, [_P(ctypes.c_int)])
@@ -406,6 +412,37 @@ def rpq_graph_load(graph=None, *, num_vertices=None, src=None, dst=None, label=N
     h = ctypes.c_void_p()
     _check(_c["rpq_graph_load"](ctypes.byref(d), ctypes.byref(h)))
     return Graph(h.value, label_names, vertex_label_names or [], int(num_vertices))
+
+
+def rpq_graph_add_label(g: Graph, name: str, src, dst, stream=None) -> int:
+    """Add a derived edge label from host (src, dst) arrays; returns its id."""
+    a = _arr(src if len(src) else [0], np.uint32)
+    b = _arr(dst if len(dst) else [0], np.uint32)
+    lid = ctypes.c_uint32()
+    _check(_c["rpq_graph_add_label"](g.h, name.encode(), a.ctypes.data, b.ctypes.data, len(src), 0, stream,
+                                     ctypes.byref(lid)))
+    g.label_names.append(name)
+    return lid.value
+
+
+def rpq_cache_closure(g: Graph, inner: Nfa, name: str, opts: Optional[rpq_eval_opts] = None, **kw) -> int:
+    """Install R(inner) as the derived label `name` (loop-cache plan)."""
+    o = opts if opts is not None else make_opts(**kw)
+    lid = ctypes.c_uint32()
+    _check(_c["rpq_cache_closure"](g.h, inner.h, name.encode(), ctypes.byref(o), ctypes.byref(lid)))
+    g.label_names.append(name)
+    return lid.value
+
+
+def rpq_eval_loop_cached(g: Graph, prefix: str, loop: str, suffix: str,
+                         opts: Optional[rpq_eval_opts] = None, **kw) -> Result:
+    """All-pairs R(prefix (loop)* suffix) with the loop-cache plan (WavePlan
+    A2; see include/rpq.h).  Same pairs as the direct plan."""
+    o = opts if opts is not None else make_opts(**kw)
+    h = ctypes.c_void_p()
+    _check(_c["rpq_eval_loop_cached"](g.h, (prefix or "").encode(), loop.encode(), (suffix or "").encode(),
+                                      ctypes.byref(o), ctypes.byref(h)))
+    return Result(h.value)
 
 
 def rpq_graph_info(g: Graph):

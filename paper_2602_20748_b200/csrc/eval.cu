@@ -37,6 +37,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cctype>
+#include <string>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -1913,7 +1916,10 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     const bool timeit = o.mode & RPQ_TIME_KERNELS;
     const uint32_t shard_count = o.shard_count ? o.shard_count : 1;
     if (o.shard_index >= shard_count) return rpq_fail(RPQ_EINVAL, "shard_index >= shard_count");
-    if (a->vocab != g->label_names)
+    // the automaton's vocabulary must be the graph's, or a prefix of it
+    // (labels added since with rpq_graph_add_label keep the old ids)
+    if (a->vocab.size() > g->label_names.size() ||
+        !std::equal(a->vocab.begin(), a->vocab.end(), g->label_names.begin()))
         return rpq_fail(RPQ_EINVAL, "automaton was compiled against a different label vocabulary");
     RPQ_CUDA_TRY(cudaSetDevice(g->device));
     cudaStream_t s = (cudaStream_t)o.cuda_stream;
@@ -3183,6 +3189,61 @@ extern "C" rpq_status rpq_eval_allpairs_stream(const rpq_graph *g, const rpq_nfa
     }
     if (total) *total = delivered;
     return RPQ_OK;
+}
+
+// Loop-cache plan (WavePlan A2: "partial query results are first
+// materialized ... and then reused in subsequent RPQ exploration"): R(inner)
+// over all of V, installed in the graph as the derived label `name`, so that
+// e.g. a (b c)* d runs as a L? d with L = R((b c)+).
+extern "C" rpq_status rpq_cache_closure(rpq_graph *g, const rpq_nfa *inner, const char *name,
+                                        const rpq_eval_opts *opts, uint32_t *label_id) {
+    rpq_result *r = nullptr;
+    rpq_status st = check_common(g, inner, &r);
+    if (st) return st;
+    rpq_eval_opts o{};
+    if (opts) o = *opts;
+    o.mode = RPQ_PAIRS | (o.mode & (RPQ_STATS | RPQ_TIME_KERNELS | RPQ_BOUNDED));
+    o.shard_index = 0;
+    o.shard_count = 1;
+    if ((st = eval_sources_device(g, inner, nullptr, 0, &o, &r)) != RPQ_OK) return st;
+    st = rpq_graph_add_label(g, name, r->cols[0], r->cols[1], r->nrows, 1, o.cuda_stream, label_id);
+    rpq_result_release(r);
+    return st;
+}
+
+// The whole loop-cache plan for all-pairs R(prefix (loop)* suffix): cache
+// R(loop+) as a fresh derived label L, then evaluate "(prefix) L? (suffix)".
+extern "C" rpq_status rpq_eval_loop_cached(rpq_graph *g, const char *prefix, const char *loop, const char *suffix,
+                                           const rpq_eval_opts *opts, rpq_result **out) {
+    if (out) *out = nullptr;
+    if (!g || !loop || !out) return rpq_fail(RPQ_EINVAL, "rpq_eval_loop_cached: NULL argument");
+    static std::atomic<uint32_t> next_id{0};
+    std::string name;
+    for (;;) {   // a label name not in the vocabulary
+        name = "__loop" + std::to_string(next_id++);
+        if (std::find(g->label_names.begin(), g->label_names.end(), name) == g->label_names.end()) break;
+    }
+    rpq_nfa *inner = nullptr, *outer = nullptr;
+    struct G2 { rpq_nfa **a, **b; ~G2() { delete *a; delete *b; } } gd{&inner, &outer};
+    size_t eo = 0;
+    const std::string lp = "(" + std::string(loop) + ")+";
+    rpq_status st = compile_regex(g->label_names, lp.c_str(), 0, &inner, &eo);
+    if (st != RPQ_OK) return st;
+    rpq_eval_opts co{};
+    if (opts) co = *opts;
+    co.mode &= ~(uint32_t)RPQ_BOUNDED;   // the closure itself is unbounded
+    if ((st = rpq_cache_closure(g, inner, name.c_str(), &co, nullptr)) != RPQ_OK) return st;
+    auto blank = [](const char *x) {
+        if (!x) return true;
+        for (; *x; ++x) if (!isspace((unsigned char)*x)) return false;
+        return true;
+    };
+    std::string q;
+    if (!blank(prefix)) q += "(" + std::string(prefix) + ") ";
+    q += name + "?";
+    if (!blank(suffix)) q += " (" + std::string(suffix) + ")";
+    if ((st = compile_regex(g->label_names, q.c_str(), 0, &outer, &eo)) != RPQ_OK) return st;
+    return rpq_eval_allpairs(g, outer, opts, out);
 }
 
 extern "C" rpq_status rpq_eval_targets(const rpq_graph *g, const rpq_nfa *a, const uint32_t *targets,

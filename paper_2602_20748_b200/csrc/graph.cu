@@ -21,7 +21,7 @@ namespace {
 __global__ void k_validate(const uint32_t *src, const uint32_t *dst, const uint16_t *lab, uint64_t ne,
                            uint32_t nv, uint32_t nl, int *bad) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < ne; i += (uint64_t)gridDim.x * blockDim.x)
-        if (src[i] >= nv || dst[i] >= nv || lab[i] >= nl) *bad = 1;
+        if (src[i] >= nv || dst[i] >= nv || (lab && lab[i] >= nl)) *bad = 1;
 }
 
 __global__ void k_label_hist(const uint16_t *lab, uint64_t ne, unsigned long long *cnt) {
@@ -122,6 +122,7 @@ extern "C" void rpq_graph_free(rpq_graph *g) {
     }
     graph_block_free(g, g->vlabel);
     graph_block_free(g, g->d_iota);
+    for (void *b : g->extra_blocks) graph_block_free(g, b);
     for (auto *e : g->prod_cache) {
         graph_block_free(g, e->d_pidx);
         delete e;
@@ -302,6 +303,123 @@ extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
     dev_available_invalidate();
     return RPQ_OK;
 #undef GTRY
+}
+
+__global__ void k_pack_pairs(const uint32_t *a, const uint32_t *b, uint64_t n, uint64_t *key) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        key[i] = ((uint64_t)a[i] << 32) | b[i];
+}
+
+// One derived label's CSR (and its transpose when the graph keeps in-edges)
+// from device pairs: pack -> radix sort -> unique -> degrees -> scan, as in
+// rpq_graph_load.
+static rpq_status build_derived_csr(rpq_graph *g, const uint32_t *ds, const uint32_t *dd, uint64_t n, bool transpose,
+                                    LabelCSR &c, cudaStream_t s) {
+    const uint32_t nv = g->nv;
+    Cleanup tmp{{}, s};
+    auto alloc = [&](size_t bytes) { void *p = dev_alloc(bytes, s); if (p) tmp.ptrs.push_back(p); return p; };
+    uint64_t *k1 = (uint64_t *)alloc(std::max<uint64_t>(n, 1) * 8), *k2 = (uint64_t *)alloc(std::max<uint64_t>(n, 1) * 8);
+    uint64_t *d_m = (uint64_t *)alloc(8), *d_fl = (uint64_t *)alloc(16);
+    uint32_t *d_mm = (uint32_t *)alloc(8), *d_md = (uint32_t *)alloc(4);
+    if (!k1 || !k2 || !d_m || !d_fl || !d_mm || !d_md) return rpq_fail(RPQ_ENOMEM, "rpq_graph_add_label: out of device memory");
+    uint32_t *off = (uint32_t *)graph_alloc(g, (nv + 1ull) * 4, s);
+    uint32_t *nbr = (uint32_t *)graph_alloc(g, std::max<uint64_t>(n, 4) * 4, s);
+    if (off) g->extra_blocks.push_back(off);
+    if (nbr) g->extra_blocks.push_back(nbr);
+    if (!off || !nbr) return rpq_fail(RPQ_ENOMEM, "rpq_graph_add_label: out of device memory (CSR)");
+    int vbits = 1;
+    while (vbits < 32 && (1ull << vbits) < nv) ++vbits;
+    RPQ_CUDA_TRY(cudaMemsetAsync(off, 0, (nv + 1ull) * 4, s));
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_m, 0, 8, s));
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_fl, 0, 16, s));
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_mm, 0xff, 4, s));
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_mm + 1, 0, 4, s));
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_md, 0, 4, s));
+    if (n) {
+        if (transpose) k_pack_pairs<<<grid_for(n), 256, 0, s>>>(dd, ds, n, k1);
+        else k_pack_pairs<<<grid_for(n), 256, 0, s>>>(ds, dd, n, k1);
+        size_t t1 = 0, t2 = 0, t3 = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, t1, k1, k2, (int64_t)n, 0, 32 + vbits, s);
+        cub::DeviceSelect::Unique(nullptr, t2, k2, k1, d_m, (int64_t)n, s);
+        cub::DeviceScan::InclusiveSum(nullptr, t3, off, off, (int64_t)nv + 1, s);
+        void *ts = alloc(std::max(t1, std::max(t2, t3)));
+        if (!ts) return rpq_fail(RPQ_ENOMEM, "rpq_graph_add_label: sort temp");
+        size_t tb = t1;
+        cub::DeviceRadixSort::SortKeys(ts, tb, k1, k2, (int64_t)n, 0, 32 + vbits, s);
+        tb = t2;
+        cub::DeviceSelect::Unique(ts, tb, k2, k1, d_m, (int64_t)n, s);
+        k_degree_nbr<<<grid_for(n), 256, 0, s>>>(k1, d_m, off, nbr, d_mm, d_fl);
+        tb = t3;
+        cub::DeviceScan::InclusiveSum(ts, tb, off, off, (int64_t)nv + 1, s);
+        k_max_deg<<<grid_for(nv), 256, 0, s>>>(off, nv, d_md);
+    }
+    uint64_t hm = 0, hfl[2] = {0, 0};
+    uint32_t hmm[2] = {0, 0}, hmd = 0;
+    RPQ_CUDA_TRY(cudaMemcpyAsync(&hm, d_m, 8, cudaMemcpyDeviceToHost, s));
+    RPQ_CUDA_TRY(cudaMemcpyAsync(hfl, d_fl, 16, cudaMemcpyDeviceToHost, s));
+    RPQ_CUDA_TRY(cudaMemcpyAsync(hmm, d_mm, 8, cudaMemcpyDeviceToHost, s));
+    RPQ_CUDA_TRY(cudaMemcpyAsync(&hmd, d_md, 4, cudaMemcpyDeviceToHost, s));
+    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    c = LabelCSR{};
+    c.off = off;
+    c.nbr = nbr;
+    c.m = n ? hm : 0;
+    c.max_deg = c.m ? hmd : 0;
+    if (c.m) {
+        c.src_min = (uint32_t)(hfl[0] >> 32);
+        c.src_max = (uint32_t)(hfl[1] >> 32);
+        c.dst_min = hmm[0];
+        c.dst_max = hmm[1];
+    }
+    return RPQ_OK;
+}
+
+extern "C" rpq_status rpq_graph_add_label(rpq_graph *g, const char *name, const uint32_t *src, const uint32_t *dst,
+                                          uint64_t n, int on_device, void *stream, uint32_t *label_id) {
+    if (!g || !name || !*name || (n && (!src || !dst))) return rpq_fail(RPQ_EINVAL, "rpq_graph_add_label: bad argument");
+    for (const auto &l : g->label_names)
+        if (l == name) return rpq_fail(RPQ_EINVAL, "rpq_graph_add_label: label '%s' exists", name);
+    if (g->label_names.size() >= 65535) return rpq_fail(RPQ_EUNSUPPORTED, "rpq_graph_add_label: too many labels");
+    if (n > 0xffffffffull) return rpq_fail(RPQ_EUNSUPPORTED, "rpq_graph_add_label: >= 2^32 edges (u32 CSR offsets)");
+    RPQ_CUDA_TRY(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    Cleanup tmp{{}, s};
+    const uint32_t *ds = src, *dd = dst;
+    if (!on_device && n) {
+        uint32_t *a = (uint32_t *)dev_alloc(n * 4, s), *b = (uint32_t *)dev_alloc(n * 4, s);
+        if (a) tmp.ptrs.push_back(a);
+        if (b) tmp.ptrs.push_back(b);
+        if (!a || !b) return rpq_fail(RPQ_ENOMEM, "rpq_graph_add_label: out of device memory");
+        RPQ_CUDA_TRY(cudaMemcpyAsync(a, src, n * 4, cudaMemcpyHostToDevice, s));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(b, dst, n * 4, cudaMemcpyHostToDevice, s));
+        ds = a;
+        dd = b;
+    }
+    int *d_bad = (int *)dev_alloc(sizeof(int), s);
+    if (!d_bad) return rpq_fail(RPQ_ENOMEM, "rpq_graph_add_label: out of device memory");
+    tmp.ptrs.push_back(d_bad);
+    int bad = 0;
+    RPQ_CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+    if (n) k_validate<<<grid_for(n), 256, 0, s>>>(ds, dd, nullptr, n, g->nv, 1, d_bad);
+    RPQ_CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+    if (bad) return rpq_fail(RPQ_EINVAL, "rpq_graph_add_label: vertex id >= num_vertices");
+    LabelCSR out_c, in_c;
+    rpq_status st = build_derived_csr(g, ds, dd, n, false, out_c, s);
+    if (st != RPQ_OK) return st;
+    const bool in_edges = g->in_csr.size() == g->csr.size() && !g->csr.empty();
+    if (in_edges && (st = build_derived_csr(g, ds, dd, n, true, in_c, s)) != RPQ_OK) return st;
+    {
+        std::lock_guard<std::mutex> lk(g->sym_mu);
+        g->csr.push_back(out_c);
+        if (in_edges) g->in_csr.push_back(in_c);
+        g->label_names.emplace_back(name);
+        g->ne += out_c.m;
+        if (!g->sym.empty()) g->sym.push_back(-1);
+    }
+    if (label_id) *label_id = (uint32_t)(g->label_names.size() - 1);
+    dev_available_invalidate();
+    return RPQ_OK;
 }
 
 extern "C" rpq_status rpq_graph_info(const rpq_graph *g, uint32_t *nv, uint64_t *ne, uint32_t *nl) {

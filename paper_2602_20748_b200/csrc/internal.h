@@ -58,6 +58,8 @@ struct rpq_graph {
     mutable uint32_t *d_iota = nullptr;  // [nv] 0, 1, ..., nv - 1
     mutable std::vector<ProdEntry *> prod_cache;
     mutable std::vector<std::pair<std::vector<uint32_t>, int>> engine_cache;   // automaton signature -> sparse?
+    // CSR blocks of labels added after load (rpq_graph_add_label)
+    std::vector<void *> extra_blocks;
 };
 // graph-owned device blocks (rpq_set_allocator at load time, else cudaMalloc)
 void *graph_alloc(const rpq_graph *g, size_t bytes, void *stream);
