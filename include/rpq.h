@@ -284,6 +284,23 @@ typedef struct {
 } crpq_query;
 rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts,
                      rpq_result **out);
+/* crpq_eval projected onto out_vars (distinct variable ids, in that column
+ * order): the distinct tuples of those variables over all homomorphisms,
+ * sorted lexicographically.  EINVAL for an empty / repeated / out-of-range
+ * list. */
+rpq_status crpq_eval_project(const rpq_graph *g, const crpq_query *q, const uint32_t *out_vars, uint32_t num_out,
+                             const rpq_eval_opts *opts, rpq_result **out);
+/* Start-in-the-middle plan (WavePlan A3/A4) for
+ * R(alpha mid beta): exploration starts at the edges of the middle
+ * expression `mid` (typically one selective label) -- alpha is traversed
+ * backwards (reversed automaton, in-edge CSR when loaded: "with transpose")
+ * and beta forwards -- and the distinct (x, y) pairs are enumerated, sorted
+ * and deduplicated (they cannot be produced in source order).  Runs as the
+ * CRPQ x -alpha-> u -mid-> w -beta-> y (RPQ_WCOJ, matching order from the
+ * middle) projected on (x, y).  Same pairs as rpq_eval_allpairs on
+ * "(alpha)(mid)(beta)".  Errors as rpq_compile / crpq_eval. */
+rpq_status rpq_eval_middle(const rpq_graph *g, const char *alpha, const char *mid, const char *beta,
+                           const rpq_eval_opts *opts, rpq_result **out);
 
 /* ------------------------------------------------------------------------
  * Results.  Pair results have 2 columns (src, dst); CRPQ results one column

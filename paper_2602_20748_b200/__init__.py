@@ -127,7 +127,7 @@ EXPORTED = [
     "rpq_device_count", "rpq_version", "rpq_shard_plan", "rpq_trim_memory",
     "rpq_nfa_reverse", "rpq_eval_targets", "rpq_eval_single_target", "rpq_eval_allpairs_stream",
     "rpq_set_allocator", "rpq_plan", "rpq_result_batches", "rpq_result_source_pe",
-    "rpq_graph_add_label", "rpq_cache_closure", "rpq_eval_loop_cached",
+    "rpq_graph_add_label", "rpq_cache_closure", "rpq_eval_loop_cached", "crpq_eval_project", "rpq_eval_middle",
 ]
 
 _c = {}
@@ -172,6 +172,10 @@ _c["rpq_result_batches"] = _proto("rpq_result_batches", _st, [_vp, _P(rpq_batch_
 _c["rpq_plan"] = _proto("rpq_plan", _st, [_vp, _vp, _P(rpq_eval_opts), _P(rpq_plan_info)])
 _c["rpq_graph_add_label"] = _proto("rpq_graph_add_label", _st, [_vp, ctypes.c_char_p, _vp, _vp, ctypes.c_uint64,
                                                                 ctypes.c_int, _vp, c_u32p])
+_c["crpq_eval_project"] = _proto("crpq_eval_project", _st, [_vp, _P(crpq_query), c_u32p, ctypes.c_uint32,
+                                                            _P(rpq_eval_opts), _P(_vp)])
+_c["rpq_eval_middle"] = _proto("rpq_eval_middle", _st, [_vp, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
+                                                        _P(rpq_eval_opts), _P(_vp)])
 _c["rpq_eval_loop_cached"] = _proto("rpq_eval_loop_cached", _st, [_vp, ctypes.c_char_p, ctypes.c_char_p,
                                                                   ctypes.c_char_p, _P(rpq_eval_opts), _P(_vp)])
 _c["rpq_cache_closure"] = _proto("rpq_cache_closure", _st, [_vp, _vp, ctypes.c_char_p, _P(rpq_eval_opts), c_u32p])
@@ -576,8 +580,18 @@ def rpq_eval_single_target(g: Graph, a: Nfa, t: int, opts: Optional[rpq_eval_opt
     return Result(h.value)
 
 
+def rpq_eval_middle(g: Graph, alpha: str, mid: str, beta: str, opts: Optional[rpq_eval_opts] = None,
+                    **kw) -> Result:
+    """Start-in-the-middle plan for R(alpha mid beta) (see include/rpq.h)."""
+    o = opts if opts is not None else make_opts(**kw)
+    h = ctypes.c_void_p()
+    _check(_c["rpq_eval_middle"](g.h, alpha.encode(), mid.encode(), beta.encode(), ctypes.byref(o),
+                                 ctypes.byref(h)))
+    return Result(h.value)
+
+
 def crpq_eval(g: Graph, var_label, var_const, atoms, distinct=(), opts: Optional[rpq_eval_opts] = None,
-              **kw) -> Result:
+              out_vars=None, **kw) -> Result:
     """var_label/var_const: per variable (-1 = any / free); atoms: list of
     (x, Nfa, y) with variable indices; distinct: list of (var, var)."""
     o = opts if opts is not None else make_opts(**kw)
@@ -599,7 +613,12 @@ def crpq_eval(g: Graph, var_label, var_const, atoms, distinct=(), opts: Optional
     q.num_distinct = len(distinct)
     q.distinct_pairs = _ptr(dp, ctypes.c_uint32)
     h = ctypes.c_void_p()
-    _check(_c["crpq_eval"](g.h, ctypes.byref(q), ctypes.byref(o), ctypes.byref(h)))
+    if out_vars is None:
+        _check(_c["crpq_eval"](g.h, ctypes.byref(q), ctypes.byref(o), ctypes.byref(h)))
+    else:
+        ov = _arr(list(out_vars) or [0], np.uint32)
+        _check(_c["crpq_eval_project"](g.h, ctypes.byref(q), _ptr(ov, ctypes.c_uint32), len(out_vars),
+                                       ctypes.byref(o), ctypes.byref(h)))
     return Result(h.value)
 
 
@@ -623,7 +642,7 @@ def rpq_result_device_view(r: Result):
     return r.device_view()
 
 
-def crpq(g: Graph, vars, atoms, var_label=None, var_const=None, distinct=(), **kw) -> Result:
+def crpq(g: Graph, vars, atoms, var_label=None, var_const=None, distinct=(), project=None, **kw) -> Result:
     """Convenience marshalling for crpq_eval: vars = names; atoms = (x, regex,
     y) with variable names; var_label = {var: vertex-label name};
     var_const = {var: vertex id}; distinct = [(var, var)]."""
@@ -635,4 +654,5 @@ def crpq(g: Graph, vars, atoms, var_label=None, var_const=None, distinct=(), **k
     for v, c in (var_const or {}).items():
         vc[idx[v]] = int(c)
     at = [(idx[x], rpq_compile(g, rx), idx[y]) for (x, rx, y) in atoms]
-    return crpq_eval(g, vl, vc, at, [(idx[a], idx[b]) for a, b in distinct], **kw)
+    ov = None if project is None else [idx[v] for v in project]
+    return crpq_eval(g, vl, vc, at, [(idx[a], idx[b]) for a, b in distinct], out_vars=ov, **kw)

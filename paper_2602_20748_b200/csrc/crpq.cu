@@ -501,10 +501,42 @@ rpq_status wcoj_join(const rpq_graph *g, const crpq_query *q, const rpq_eval_opt
 
 }  // namespace
 
+// rows differing from the previous one (rows sorted): the distinct projection
+__global__ void k_row_changed(const uint32_t *const *cols, uint32_t ncols, uint64_t n, uint8_t *flag) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        bool d = i == 0;
+        for (uint32_t c = 0; c < ncols && !d; ++c) d = cols[c][i] != cols[c][i - 1];
+        flag[i] = d;
+    }
+}
+
+static rpq_status crpq_impl(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts_in,
+                            const std::vector<uint32_t> &outv, rpq_result **out);
+
 extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts_in,
                                 rpq_result **out) {
     if (out) *out = nullptr;
     if (!g || !q || !out) return rpq_fail(RPQ_EINVAL, "crpq_eval: NULL argument");
+    std::vector<uint32_t> all(q->num_vars);
+    for (uint32_t v = 0; v < q->num_vars; ++v) all[v] = v;
+    return crpq_impl(g, q, opts_in, all, out);
+}
+
+extern "C" rpq_status crpq_eval_project(const rpq_graph *g, const crpq_query *q, const uint32_t *out_vars,
+                                        uint32_t num_out, const rpq_eval_opts *opts_in, rpq_result **out) {
+    if (out) *out = nullptr;
+    if (!g || !q || !out || !out_vars || num_out == 0) return rpq_fail(RPQ_EINVAL, "crpq_eval_project: bad argument");
+    std::vector<uint32_t> ov(out_vars, out_vars + num_out);
+    for (uint32_t i = 0; i < num_out; ++i) {
+        if (ov[i] >= q->num_vars) return rpq_fail(RPQ_EINVAL, "crpq_eval_project: output variable %u", ov[i]);
+        for (uint32_t j = 0; j < i; ++j)
+            if (ov[j] == ov[i]) return rpq_fail(RPQ_EINVAL, "crpq_eval_project: repeated output variable");
+    }
+    return crpq_impl(g, q, opts_in, ov, out);
+}
+
+static rpq_status crpq_impl(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts_in,
+                            const std::vector<uint32_t> &outv, rpq_result **out) {
     const uint32_t nvars = q->num_vars, natoms = q->num_atoms;
     if (nvars == 0 || nvars > RPQ_MAX_COLS) return rpq_fail(RPQ_EINVAL, "crpq_eval: 1..%d variables", RPQ_MAX_COLS);
     if (natoms == 0 || !q->atom_x || !q->atom_y || !q->atom_nfa)
@@ -762,20 +794,22 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
         if (st != RPQ_OK) return st;
     }
 
-    // ---- lexicographic order in variable order: stable LSD radix passes ----
+    // ---- lexicographic order in output-variable order: stable LSD radix
+    // passes; a projection (crpq_eval_project) then keeps distinct rows ----
+    const uint32_t nout = (uint32_t)outv.size();
+    const bool project = nout < nvars;
     rpq_result *res = new rpq_result();
     res->stream = (void *)s;
     res->alloc_snap = alloc_snapshot();
     res->device = g->device;
-    res->ncols = nvars;
+    res->ncols = nout;
     res->nrows = T.n;
     res->count = T.n;
     auto fail = [&](rpq_status st) { rpq_result_release(res); return st; };
-    for (uint32_t v = 0; v < nvars; ++v) {
-        if (!dev_alloc_to(res->cols[v], std::max<uint64_t>(T.n, 1) * 4, s)) {
-            cudaGetLastError();
-            return fail(rpq_fail(RPQ_ENOMEM, "crpq: out of device memory (result)"));
-        }
+    std::vector<uint32_t *> sorted(nout);
+    for (uint32_t k = 0; k < nout; ++k) {
+        sorted[k] = (uint32_t *)P.get(std::max<uint64_t>(T.n, 1) * 4);
+        if (!sorted[k]) return fail(rpq_fail(RPQ_ENOMEM, "crpq: out of device memory (result)"));
     }
     if (T.n) {
         uint32_t *perm = (uint32_t *)P.get(T.n * 4), *perm2 = (uint32_t *)P.get(T.n * 4);
@@ -785,14 +819,32 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
         void *tmp = P.get(tb);
         if (!perm || !perm2 || !key || !key2 || !tmp) return fail(rpq_fail(RPQ_ENOMEM, "crpq: oom"));
         k_iota32<<<grid_for(T.n), 256, 0, s>>>(perm, T.n);
-        for (int v = (int)nvars - 1; v >= 0; --v) {
-            const int c = T.col_of((uint32_t)v);
+        for (int k = (int)nout - 1; k >= 0; --k) {
+            const int c = T.col_of(outv[k]);
             k_gather<<<grid_for(T.n), 256, 0, s>>>(T.cols[c], perm, T.n, key);
             cub::DeviceRadixSort::SortPairs(tmp, tb, key, key2, perm, perm2, (int64_t)T.n, 0, 32, s);
             std::swap(perm, perm2);
         }
-        for (uint32_t v = 0; v < nvars; ++v)
-            k_gather<<<grid_for(T.n), 256, 0, s>>>(T.cols[T.col_of(v)], perm, T.n, res->cols[v]);
+        for (uint32_t k = 0; k < nout; ++k)
+            k_gather<<<grid_for(T.n), 256, 0, s>>>(T.cols[T.col_of(outv[k])], perm, T.n, sorted[k]);
+    }
+    uint64_t nres = T.n;
+    if (project && nres) {
+        uint8_t *flag = (uint8_t *)P.get(nres);
+        uint32_t **d_c = (uint32_t **)P.get(nout * sizeof(void *));
+        if (!flag || !d_c) return fail(rpq_fail(RPQ_ENOMEM, "crpq: oom"));
+        RPQ_CUDA_TRY(cudaMemcpyAsync(d_c, sorted.data(), nout * sizeof(void *), cudaMemcpyHostToDevice, s));
+        k_row_changed<<<grid_for(nres), 256, 0, s>>>(d_c, nout, nres, flag);
+        rpq_status cs = compact(P, sorted, nres, flag, s);
+        if (cs != RPQ_OK) return fail(cs);
+    }
+    res->nrows = res->count = nres;
+    for (uint32_t k = 0; k < nout; ++k) {
+        if (!dev_alloc_to(res->cols[k], std::max<uint64_t>(nres, 1) * 4, s)) {
+            cudaGetLastError();
+            return fail(rpq_fail(RPQ_ENOMEM, "crpq: out of device memory (result)"));
+        }
+        if (nres) RPQ_CUDA_TRY(cudaMemcpyAsync(res->cols[k], sorted[k], nres * 4, cudaMemcpyDeviceToDevice, s));
     }
     cudaEventRecord(e1, s);
     cudaError_t ce = cudaStreamSynchronize(s);
@@ -802,8 +854,47 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
     cudaEventDestroy(e1);
     if (ce != cudaSuccess) return fail(rpq_fail(RPQ_ECUDA, "crpq: %s", cudaGetErrorString(ce)));
     ST.total_ms = ms;
-    ST.count = T.n;
+    ST.count = nres;
     res->stats = ST;
     *out = res;
     return RPQ_OK;
+}
+
+// Start-in-the-middle plan (WavePlan A3/A4): R(alpha m
+// beta) for a middle label m, explored from the m-edges outwards -- alpha
+// backwards (reversed automaton over in-edges, "with transpose") from the
+// sources of m-edges, beta forwards from their targets -- then joined on the
+// middle edge and projected to distinct (x, y).  The pairs cannot come out
+// in source order during exploration ("result pairs cannot be confirmed in
+// order of start vertices"), so they are enumerated, then sorted + deduped.
+// Executed as the CRPQ x -alpha-> u, u -m-> w, w -beta-> y with the
+// worst-case-optimal join (its matching order starts at u, w: the middle).
+extern "C" rpq_status rpq_eval_middle(const rpq_graph *g, const char *alpha, const char *mid, const char *beta,
+                                      const rpq_eval_opts *opts, rpq_result **out) {
+    if (out) *out = nullptr;
+    if (!g || !alpha || !mid || !beta || !out) return rpq_fail(RPQ_EINVAL, "rpq_eval_middle: NULL argument");
+    rpq_nfa *na = nullptr, *nm = nullptr, *nb = nullptr;
+    struct G3 { rpq_nfa **a, **b, **c; ~G3() { delete *a; delete *b; delete *c; } } gd{&na, &nm, &nb};
+    size_t eo = 0;
+    rpq_status st;
+    if ((st = compile_regex(g->label_names, alpha, 0, &na, &eo)) != RPQ_OK) return st;
+    if ((st = compile_regex(g->label_names, mid, 0, &nm, &eo)) != RPQ_OK) return st;
+    if ((st = compile_regex(g->label_names, beta, 0, &nb, &eo)) != RPQ_OK) return st;
+    const int32_t vl[4] = {-1, -1, -1, -1};
+    const int64_t vc[4] = {-1, -1, -1, -1};
+    const uint32_t ax[3] = {0, 1, 2}, ay[3] = {1, 2, 3};
+    const rpq_nfa *an[3] = {na, nm, nb};
+    crpq_query q{};
+    q.num_vars = 4;
+    q.var_label = vl;
+    q.var_const = vc;
+    q.num_atoms = 3;
+    q.atom_x = ax;
+    q.atom_y = ay;
+    q.atom_nfa = an;
+    rpq_eval_opts o{};
+    if (opts) o = *opts;
+    o.mode |= RPQ_WCOJ;
+    const uint32_t ov[2] = {0, 3};
+    return crpq_eval_project(g, &q, ov, 2, &o, out);
 }

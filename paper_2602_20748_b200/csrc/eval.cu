@@ -121,6 +121,7 @@ struct Ctrl {                  // per-level device counters / flags
     uint32_t ntouched;         // entries of LevelArgs::TL
     uint32_t pcur[2];          // pull-level task cursor per parity
     uint32_t hcur;             // hub-record cursor (reset per level and before the seed hub launch)
+    uint32_t blevel;           // levels of the current batch (reset by k_seed; the length bound)
 };
 
 // One BFS level over the rows whose activity bit is set in (Xcur, XBcur).
@@ -137,7 +138,7 @@ struct LevelArgs {
     // consumed), Mark = Vis (written only by row owners), Disc = N[par ^ 1].
     uint64_t *Front, *Mark, *Disc;
     uint32_t bounded;
-    uint32_t level_lim;        // last level (ctrl->levels) that may expand; ~0u = unbounded
+    uint32_t level_lim;        // last level of a batch (ctrl->blevel) that may expand; ~0u = unbounded
     uint32_t *Xcur, *Xnext;    // chunk-activity bitmaps, one word per (row, xw)
     uint32_t *XBcur, *XBnext;  // block bitmaps: one bit per 32 X words
     uint64_t nxwords;          // rows * nxw
@@ -237,6 +238,7 @@ __global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
         p.ctrl->nhub_recs = 0;
         p.ctrl->hcur = 0;
         p.ctrl->levels += 1;
+        p.ctrl->blevel += 1;
     }
     if (p.pull_mode)   // the previous level's filter, free now: this level accumulates into it
         for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < p.nw; i += (uint64_t)gridDim.x * blockDim.x)
@@ -396,7 +398,7 @@ __global__ void k_level_end(Ctrl *ctrl, cudaGraphConditionalHandle h) {
 // independent visited-word loads outstanding.
 //   m = f & ~Vis[t];  Vis[t] |= m (red, same sector as the test load, so it
 //   hits L2);  X/XB activity of t (red).
-template <int KC, bool STATS>
+template <int KC, bool STATS, bool BND = false>
 __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S, uint32_t q2,
                                              const uint32_t *__restrict__ nbr, uint32_t beg, uint32_t end,
                                              const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
@@ -437,7 +439,7 @@ __device__ __forceinline__ void expand_edges(const LevelArgs &p, const Layout &S
                 for (int k = 0; k < KC; ++k) {
                     const uint64_t m = (e0 + e < cnt) ? (f[k] & ~b.vis[e][k]) : 0ull;
                     if (m) {
-                        red_or64(p.Disc + rb + ckk[k], m);
+                        red_or64((BND ? p.Disc : p.Vis) + rb + ckk[k], m);
                         lm |= 1u << ((bits >> (8 * k)) & 0xffu);
                         if (STATS) st[S_N_RED]++;
                     }
@@ -485,20 +487,20 @@ __device__ __forceinline__ void flush_stats(unsigned long long *st, unsigned lon
     }
 }
 
-template <bool STATS>
+template <bool STATS, bool BND = false>
 __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const Layout &S, uint32_t q2,
                                                const uint32_t *nbr, uint32_t beg, uint32_t end,
                                                const uint64_t (&f)[KGRP], uint64_t bits, uint32_t xw, int lane,
                                                unsigned long long *st, bool &act, bool live) {
     if constexpr (KGRP > 4) {
         if (nk > 4) {
-            expand_edges<8, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+            expand_edges<8, STATS, BND>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
             return;
         }
     }
-    if (nk > 2) expand_edges<4, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
-    else if (nk > 1) expand_edges<2, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
-    else expand_edges<1, STATS>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+    if (nk > 2) expand_edges<4, STATS, BND>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+    else if (nk > 1) expand_edges<2, STATS, BND>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
+    else expand_edges<1, STATS, BND>(p, S, q2, nbr, beg, end, f, bits, xw, lane, st, act, live);
 }
 
 // Main level kernel: a warp owns one active X word = one row and up to 32 of
@@ -506,11 +508,11 @@ __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const
 // f = Vis & ~Done; Done |= f) and then expanded along every automaton
 // transition of the row's state.  Work units (32 X words = one XB bit) are
 // interleaved over warps.
-template <bool STATS>
+template <bool STATS, bool BND = false>
 __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, const Layout *__restrict__ Sg,
                                                                const LevelArgs p) {
     if (level_pull(p)) return;                 // bottom-up level: k_pull_prep + k_pull
-    if (*(volatile const uint32_t *)&p.ctrl->levels > p.level_lim) return;   // length bound reached
+    if (BND && *(volatile const uint32_t *)&p.ctrl->blevel > p.level_lim) return;   // length bound reached
     __shared__ Layout S;
     __shared__ unsigned long long actS[ACT_SMEM_WORDS];
     load_layout(S, Sg, A.nq);
@@ -579,16 +581,16 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                     nk += has;
                     bits |= (uint64_t)bt << (8 * k);
                     const bool ok = has && lane_ok && xw * 32u * p.cw + bt * p.cw + lane < p.nw;
-                    f[k] = ok ? ld_cg(p.Front + rb + bt * p.cw) : 0ull;
-                    dd[k] = ok ? p.Mark[rb + bt * p.cw] : ~0ull;
+                    f[k] = ok ? ld_cg((BND ? p.Front : p.Vis) + rb + bt * p.cw) : 0ull;
+                    dd[k] = ok ? (BND ? p.Mark : p.Done)[rb + bt * p.cw] : ~0ull;
                 }
 #pragma unroll
                 for (int k = 0; k < KGRP; ++k) {
                     const uint32_t bt = (uint32_t)(bits >> (8 * k)) & 0xffu;
-                    if (p.bounded && f[k]) p.Front[rb + bt * p.cw] = 0ull;   // N[par] consumed
+                    if (BND && f[k]) p.Front[rb + bt * p.cw] = 0ull;   // N[par] consumed
                     f[k] &= ~dd[k];
                     if (f[k]) {
-                        p.Mark[rb + bt * p.cw] = dd[k] | f[k];
+                        (BND ? p.Mark : p.Done)[rb + bt * p.cw] = dd[k] | f[k];
                         // sources of this frontier word may gain bits next level
                         if (p.pull_mode) act_or(actS, p.ActNext, (uint32_t)(rb - row * p.nw) + bt * p.cw, f[k]);
                         if (STATS) st[S_WORD_ITEMS]++;
@@ -654,7 +656,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                                 p.hrecs[r + sg] = HubRec{0u, 0u, 0u, 0u};
                         }
                     }
-                    dispatch_edges<STATS>(nk, p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act,
+                    dispatch_edges<STATS, BND>(nk, p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act,
                                           A.toff[A.tto[t] + 1] > A.toff[A.tto[t]]);
                 }
             }
@@ -666,10 +668,10 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
 }
 
 // Deferred long rows: a warp per HUB_EDGES-edge segment.
-template <bool STATS>
+template <bool STATS, bool BND = false>
 __global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A, const Layout *__restrict__ Sg,
                                                                    const LevelArgs p) {
-    if (*(volatile const uint32_t *)&p.ctrl->levels > p.level_lim) return;   // length bound reached
+    if (BND && *(volatile const uint32_t *)&p.ctrl->blevel > p.level_lim) return;   // length bound reached
     __shared__ Layout S;
     load_layout(S, Sg, A.nq);
     const int lane = threadIdx.x & 31;
@@ -692,7 +694,7 @@ __global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A
         uint64_t f[KGRP];
 #pragma unroll
         for (int k = 0; k < KGRP; ++k) f[k] = p.hubF[((uint64_t)r.hitem * KGRP + k) * 32 + lane];
-        dispatch_edges<STATS>((int)h.nk, p, S, A.tto[r.t], A.nbr[A.tslot[r.t]], r.beg, r.end, f, h.bits, h.xw, lane,
+        dispatch_edges<STATS, BND>((int)h.nk, p, S, A.tto[r.t], A.nbr[A.tslot[r.t]], r.beg, r.end, f, h.bits, h.xw, lane,
                               st, act, A.toff[A.tto[r.t] + 1] > A.toff[A.tto[r.t]]);
     }
     if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
@@ -968,6 +970,7 @@ __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const 
         ctrl->ucnt[0] = ctrl->ucnt[1] = 0;
         ctrl->ucur[0] = ctrl->ucur[1] = 0;
         ctrl->ntouched = 0;
+        ctrl->blevel = 0;
     }
 }
 
@@ -1021,7 +1024,7 @@ __global__ void k_xb_from_x(const uint32_t *X, uint64_t nxwords, uint32_t *XB) {
 // Level 0 without q0 rows: a warp per batch source expands its single bit
 // along q0's transitions straight into N / X / XB of the parity-0 level.
 // p must be the parity-1 argument set (its "next" buffers are parity 0).
-template <bool STATS>
+template <bool STATS, bool BND = false>
 __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layout *__restrict__ Sg,
                                                      const LevelArgs p, const uint32_t *__restrict__ cand,
                                                      const uint32_t *__restrict__ pidx, uint64_t b0, uint32_t nb,
@@ -1071,7 +1074,7 @@ __global__ void __launch_bounds__(256) k_seed_expand(const DevAuto A, const Layo
                         p.hrecs[r + sg] = HubRec{0u, 0u, 0u, 0u};
             }
             if (end > beg)
-                expand_edges<1, STATS>(p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act,
+                expand_edges<1, STATS, BND>(p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act,
                                        A.toff[A.tto[t] + 1] > A.toff[A.tto[t]]);
         }
     }
@@ -1808,7 +1811,7 @@ struct LevelGraph {
     }
 };
 
-template <bool STATS>
+template <bool STATS, bool BND>
 cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg, const LevelArgs &P0,
                               const LevelArgs &P1, int grid, int hgrid, uint64_t nxbwords, bool hub) {
     cudaError_t e;
@@ -1852,14 +1855,14 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
     const bool pull = P0.pull_mode != 0;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u0)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r0)) != cudaSuccess) return e;
-    if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a0)) != cudaSuccess) return e;
+    if ((e = add((void *)k_level<STATS, BND>, dim3(grid), dim3(256), a0)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a0)) != cudaSuccess) return e;
-    if (hub && (e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
+    if (hub && (e = add((void *)k_level_hub<STATS, BND>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u1)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r1)) != cudaSuccess) return e;
-    if ((e = add((void *)k_level<STATS>, dim3(grid), dim3(256), a1)) != cudaSuccess) return e;
+    if ((e = add((void *)k_level<STATS, BND>, dim3(grid), dim3(256), a1)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a1)) != cudaSuccess) return e;
-    if (hub && (e = add((void *)k_level_hub<STATS>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
+    if (hub && (e = add((void *)k_level_hub<STATS, BND>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_end, dim3(1), dim3(1), m1)) != cudaSuccess) return e;
     return cudaGraphInstantiate(&LG.exec, LG.g, 0);
 }
@@ -1876,13 +1879,17 @@ rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &
         k_units<<<ugrid, 256, 0, s>>>(P, nxbwords);
         if (P.pull_mode) k_pull_prep<<<148 * 8, 256, 0, s>>>(A, P);
         if (stats) {
-            k_level<true><<<grid, 256, 0, s>>>(A, Sg, P);
+            if (P.bounded) k_level<true, true><<<grid, 256, 0, s>>>(A, Sg, P);
+            else k_level<true><<<grid, 256, 0, s>>>(A, Sg, P);
             if (P.pull_mode) k_pull<true><<<148 * 8, 256, 0, s>>>(A, Sg, P);
-            if (hub) k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
+            if (hub && P.bounded) k_level_hub<true, true><<<hgrid, 256, 0, s>>>(A, Sg, P);
+            else if (hub) k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
         } else {
-            k_level<false><<<grid, 256, 0, s>>>(A, Sg, P);
+            if (P.bounded) k_level<false, true><<<grid, 256, 0, s>>>(A, Sg, P);
+            else k_level<false><<<grid, 256, 0, s>>>(A, Sg, P);
             if (P.pull_mode) k_pull<false><<<148 * 8, 256, 0, s>>>(A, Sg, P);
-            if (hub) k_level_hub<false><<<hgrid, 256, 0, s>>>(A, Sg, P);
+            if (hub && P.bounded) k_level_hub<false, true><<<hgrid, 256, 0, s>>>(A, Sg, P);
+            else if (hub) k_level_hub<false><<<hgrid, 256, 0, s>>>(A, Sg, P);
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(h_flag, &P.ctrl->active[par ^ 1], 4, cudaMemcpyDeviceToHost, s));
         RPQ_CUDA_TRY(cudaStreamSynchronize(s));
@@ -2656,8 +2663,11 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         } else {
             cache.lg.reset();
             auto lg = std::make_unique<LevelGraph>();
-            cudaError_t ge = stats ? build_level_graph<true>(*lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub)
-                                   : build_level_graph<false>(*lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub);
+            cudaError_t ge =
+                stats ? (bounded ? build_level_graph<true, true>(*lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub)
+                                 : build_level_graph<true, false>(*lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub))
+                      : (bounded ? build_level_graph<false, true>(*lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub)
+                                 : build_level_graph<false, false>(*lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub));
             if (ge != cudaSuccess) {   // fall back to the host-driven loop
                 cudaGetLastError();
                 if (lg->exec) cudaGraphExecDestroy(lg->exec);
@@ -2765,9 +2775,15 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             const int sg = grid_for((uint64_t)nb * 32, 256, 148 * 8);
             const int seed_lanes = getenv("RPQ_SEED_WARPS") ? 0 : 1;
             if (seed_lanes) k_seed_lanes<<<grid_for(nb), 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb);
-            if (stats) {
+            if (stats && bounded) {
+                k_seed_expand<true, true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb, seed_lanes);
+                if (need_hub) k_level_hub<true, true><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
+            } else if (stats) {
                 k_seed_expand<true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb, seed_lanes);
                 if (need_hub) k_level_hub<true><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
+            } else if (bounded) {
+                k_seed_expand<false, true><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb, seed_lanes);
+                if (need_hub) k_level_hub<false, true><<<hgrid, 256, 0, s>>>(A, d_layout, P1);
             } else {
                 k_seed_expand<false><<<sg, 256, 0, s>>>(A, d_layout, P1, cand, pidx, b0, nb, seed_lanes);
                 if (need_hub) k_level_hub<false><<<hgrid, 256, 0, s>>>(A, d_layout, P1);

@@ -26,6 +26,7 @@ def need_gpu():
 def _hub_graph(nv, ne, seed, hub_edges=1500):
     g = synth.random_graph(nv, ne, 3, seed=seed)
     rng = np.random.default_rng(seed)
+    hub_edges = min(hub_edges, nv)
     hd = rng.choice(nv, hub_edges, replace=False).astype(np.uint32)
     return synth.Graph(nv, np.concatenate([g.src, np.full(hub_edges, 7, np.uint32)]),
                        np.concatenate([g.dst, hd]), np.concatenate([g.label, np.ones(hub_edges, np.uint16)]),

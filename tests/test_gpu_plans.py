@@ -62,3 +62,32 @@ def test_derived_label_matches_loaded():
         R.rpq_graph_add_label(G, "x", s, d)            # duplicate name
     with pytest.raises(R.RPQError):
         R.rpq_graph_add_label(G, "y", np.array([5000], np.uint32), np.array([0], np.uint32))
+
+
+@pytest.mark.parametrize("ie", [False, True])
+@pytest.mark.parametrize("alpha,mid,beta", [("a*", "b", "c*"), ("(a|c)+", "d", "a b*"), ("a", "b", "c")])
+def test_start_in_the_middle_equals_direct(alpha, mid, beta, ie):
+    """WavePlan A3/A4: R(alpha mid beta) explored from the middle
+    edges outwards, enumerated then deduplicated -- the same pairs as O1."""
+    g = synth.random_graph(1500, 4500, 4, seed=11)
+    G = R.rpq_graph_load(g, in_edges=ie)
+    rx = f"({alpha}) ({mid}) ({beta})"
+    o = oracle.allpairs(g, rx)
+    got = R.rpq_eval_middle(G, alpha, mid, beta)
+    assert np.array_equal(got.rows(), sorted_pairs(o["src"], o["dst"])), rx
+    assert got.count == len(o["src"])
+
+
+def test_crpq_projection():
+    """crpq_eval_project: distinct projections of the CRPQ tuples, sorted."""
+    g = synth.random_graph(300, 1200, 3, seed=2)
+    G = R.rpq_graph_load(g, in_edges=True)
+    atoms = [("x", "a", "y"), ("y", "b*", "z"), ("x", "c", "z")]
+    full = R.crpq(G, ["x", "y", "z"], atoms).rows()
+    for proj in (["x", "z"], ["z"], ["y", "x"]):
+        idx = [["x", "y", "z"].index(v) for v in proj]
+        want = np.unique(full[:, idx], axis=0) if len(full) else np.zeros((0, len(idx)), np.uint32)
+        got = R.crpq(G, ["x", "y", "z"], atoms, project=proj).rows()
+        assert np.array_equal(got, want), proj
+        got_w = R.crpq(G, ["x", "y", "z"], atoms, project=proj, mode=R.RPQ_WCOJ).rows()
+        assert np.array_equal(got_w, want), proj
