@@ -30,19 +30,21 @@ G = R.rpq_graph_load(g, stream=s.cuda_stream, in_edges=os.environ.get("TV_IN_EDG
 tag = os.path.basename(os.environ.get("RPQ_LIB_PATH", "librpq.so"))
 for rx in qs:
     a = R.rpq_compile(G, rx)
-    R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT, stream=s.cuda_stream, shard_count=shards)
+    B = R.rpq_plan(G, a, stream=s.cuda_stream)["batch_sources"] if shards > 1 else 0
+    R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT, stream=s.cuda_stream, shard_count=shards, batch_sources=B)
     best = None
     for _ in range(3 if not wl.startswith("rmat") else 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_TIME_KERNELS, stream=s.cuda_stream,
-                                shard_count=shards)
+                                shard_count=shards, batch_sources=B)
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t0) * 1e3
         st = r.stats()
         if best is None or dt < best[0]:
             best = (dt, st["expand_ms"], r.count)
-    sp = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=s.cuda_stream, shard_count=shards).stats()
+    sp = R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT | R.RPQ_STATS, stream=s.cuda_stream, shard_count=shards,
+                             batch_sources=B).stats()
     print(f"{tag:28s} {rx:10s} total_ms={best[0]:9.2f} loop_ms={best[1]:9.2f} count={best[2]} "
           f"PE={sp['product_edges']:.4e} pull_levels={sp['pull_levels']} levels={sp['levels']} "
           f"pull_loads={sp['pull_loads']:.3e} pull_words={sp['pull_words']:.3e} adv_words={sp['adv_words']:.3e} "
