@@ -16,7 +16,10 @@ G = R.rpq_graph_load(g, stream=s)
 for rx in bench.WORKLOADS[wl]["queries"]:
     a = R.rpq_compile(G, rx)
     mode = R.RPQ_COUNT if os.environ.get("PROF_NOSTATS") else R.RPQ_COUNT | R.RPQ_STATS
-    r = R.rpq_eval_allpairs(G, a, mode=mode, stream=s, shard_index=0, shard_count=shards)
+    if os.environ.get("PROF_PAIRS"):
+        mode = R.RPQ_PAIRS
+    B = R.rpq_plan(G, a, stream=s)["batch_sources"] if shards > 1 else 0
+    r = R.rpq_eval_allpairs(G, a, mode=mode, stream=s, shard_index=0, shard_count=shards, batch_sources=B)
     torch.cuda.synchronize()
     st = r.stats()
     print(wl, rx, r.count, st["levels"], st["batches"], st["batch_sources"], flush=True)
