@@ -58,7 +58,7 @@ constexpr int MAXQ = RPQ_MAX_STATES;
 constexpr int MAXT = RPQ_MAX_TRANSITIONS;
 constexpr int MAXL = RPQ_MAX_QUERY_LABELS;
 constexpr uint32_t HUB_EDGES = 512;      // edges per hub segment
-constexpr int TILE_V = 1024;             // vertices per extraction tile
+constexpr int TILE_V = 512;              // vertices per extraction tile
 constexpr int NSTAT = 14;
 #ifndef RPQ_LEVEL_MINB
 #define RPQ_LEVEL_MINB 5
@@ -122,7 +122,17 @@ struct Ctrl {                  // per-level device counters / flags
     uint32_t pcur[2];          // pull-level task cursor per parity
     uint32_t hcur;             // hub-record cursor (reset per level and before the seed hub launch)
     uint32_t blevel;           // levels of the current batch (reset by k_seed; the length bound)
+    uint32_t txw;              // TX words that became non-zero in this batch (touched rows x 32 chunks)
 };
+
+// Clear / count a finished batch through its touched sets rather than
+// densely?  Yes when few 32-X-word units were touched, or few X words (a
+// row's 32-chunk block) even if most units were: R-MAT rows of vertices
+// without in-edges under the query's labels are never touched, but they
+// interleave with touched ones in every unit.
+__device__ __forceinline__ bool sparse_batch(const Ctrl *c, uint64_t nunits, uint64_t nxwords) {
+    return (uint64_t)c->ntouched * 4 <= nunits || (uint64_t)c->txw * 2 <= nxwords;
+}
 
 // One BFS level over the rows whose activity bit is set in (Xcur, XBcur).
 //   row r = (state q, vertex v); word (r, col) holds 64 sources' bits.
@@ -295,7 +305,7 @@ __global__ void k_units(const LevelArgs p, uint64_t nxbwords) {
 // clean without a dense memset of the whole state.
 __global__ void k_clear_touched(const LevelArgs p, uint64_t nunits, int force_dense) {
     const uint32_t ntl = p.ctrl->ntouched;
-    if (force_dense || (uint64_t)ntl * 4 > nunits) return;      // dense: k_clear_dense does it
+    if (force_dense || !sparse_batch(p.ctrl, nunits, p.nxwords)) return;      // dense: k_clear_dense does it
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -341,7 +351,7 @@ __device__ __forceinline__ uint32_t prod_deg(const DevAuto &A, int q, uint32_t v
 __global__ void k_count_touched(const DevAuto A, const Layout S, const LevelArgs p, uint64_t nunits,
                                 unsigned long long *total, int force_dense, unsigned long long *pe = nullptr) {
     const uint32_t ntl = p.ctrl->ntouched;
-    if (force_dense || (uint64_t)ntl * 4 > nunits) return;      // dense batch: k_count_total counts
+    if (force_dense || !sparse_batch(p.ctrl, nunits, p.nxwords)) return;      // dense batch: k_count_total counts
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -541,9 +551,16 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
         const bool mine = (lane / part_lanes) == (int)(tk & ((1u << ls) - 1u));
         const uint64_t xi_l = u * 32 + lane;
         const uint32_t xl = (mine && xi_l < p.nxwords) ? __ldcg(p.Xcur + xi_l) : 0u;
+        bool fresh = false;
         if (xl) {
             p.Xcur[xi_l] = 0u;
-            p.TX[xi_l] |= xl;          // single owner per level; levels are ordered
+            const uint32_t t0 = p.TX[xi_l];
+            p.TX[xi_l] = t0 | xl;      // single owner per level; levels are ordered
+            fresh = t0 == 0u;
+        }
+        {
+            const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+            if (fm && lane == 0) atomicAdd(&p.ctrl->txw, (uint32_t)__popc(fm));
         }
         unsigned todo = __ballot_sync(0xffffffffu, xl != 0);
         while (todo) {
@@ -727,9 +744,16 @@ __global__ void k_pull_prep(const DevAuto A, const LevelArgs p) {
         const uint64_t u = p.ulist[ui];
         const uint64_t xi_l = u * 32 + lane;
         const uint32_t xl = xi_l < p.nxwords ? __ldcg(p.Xcur + xi_l) : 0u;
+        bool fresh = false;
         if (xl) {
             p.Xcur[xi_l] = 0u;
-            p.TX[xi_l] |= xl;
+            const uint32_t t0 = p.TX[xi_l];
+            p.TX[xi_l] = t0 | xl;
+            fresh = t0 == 0u;
+        }
+        {
+            const unsigned fm = __ballot_sync(0xffffffffu, fresh);
+            if (fm && lane == 0) atomicAdd(&p.ctrl->txw, (uint32_t)__popc(fm));
         }
         unsigned todo = __ballot_sync(0xffffffffu, xl != 0);
         while (todo) {
@@ -971,6 +995,7 @@ __global__ void k_seed(const Layout S, const uint32_t *__restrict__ cand, const 
         ctrl->ucur[0] = ctrl->ucur[1] = 0;
         ctrl->ntouched = 0;
         ctrl->blevel = 0;
+        ctrl->txw = 0;
     }
 }
 
@@ -1409,7 +1434,7 @@ __global__ void k_batch_bounds(const uint32_t *pidx, const uint32_t *cand, uint6
 // large fraction of it (device-side decision: no host round trip).
 __global__ void k_clear_dense(uint64_t *Vis, uint64_t *Done, uint64_t words, uint32_t *TX, uint64_t nxwords,
                               uint32_t *TU, uint64_t ntu, const Ctrl *ctrl, uint64_t nunits, int force_dense) {
-    if (!force_dense && (uint64_t)ctrl->ntouched * 4 <= nunits) return;
+    if (!force_dense && sparse_batch(ctrl, nunits, nxwords - 32)) return;
     const uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = i0; i < words; i += st) { Vis[i] = 0; Done[i] = 0; }
     for (uint64_t i = i0; i < nxwords; i += st) TX[i] = 0;
@@ -1484,8 +1509,8 @@ __device__ __forceinline__ uint64_t ans_word(const DevAuto &A, const Layout &S, 
 // final (e.g. (a|b)*c*).  [vlo, vlo + vn) must then cover every state's range.
 __global__ void k_count_total(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
                               uint32_t nw, unsigned long long *total, const Ctrl *ctrl, uint64_t nunits,
-                              int force_dense, unsigned long long *pe = nullptr) {
-    if (!force_dense && ctrl && (uint64_t)ctrl->ntouched * 4 <= nunits) return;   // sparse: k_count_touched counts
+                              uint64_t nxwords, int force_dense, unsigned long long *pe = nullptr) {
+    if (!force_dense && ctrl && sparse_batch(ctrl, nunits, nxwords)) return;   // sparse: k_count_touched counts
     const int lane = threadIdx.x & 31;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
@@ -1612,20 +1637,26 @@ __global__ void k_fill_eps(unsigned long long *cand_cnt, uint64_t n, unsigned lo
         cand_cnt[j] = val;
 }
 
-// Write sorted (src, dst) pairs.  A warp takes one (1024-vertex tile, word)
-// task = 64 sources: (1) ballot transposes give, per source, 32 masks of 32
-// vertices (shared memory); (2) per source, the warp walks its masks in
-// vertex order and stores each block's targets contiguously.  Each source's
-// tile run is contiguous (start + per-tile scan), so every output sector is
-// written whole by one warp at one time (per-bit scattered writes across 256
-// sources kept ~10^6 partial runs open and doubled the DRAM traffic through
-// L2 evictions).
+// Write sorted (src, dst) pairs.  A warp takes one (TILE_V-vertex tile,
+// word) task = 64 sources: (1) ballot transposes give, per source, the masks
+// of the tile's 32-vertex blocks (shared memory); (2) per source, the warp
+// walks its masks in vertex order storing every block's targets
+// contiguously.  Each source's tile run is contiguous (start + per-tile
+// scan), so every output sector is written whole by one warp at one time
+// (per-bit scattered writes across 256 sources kept ~10^6 partial runs open
+// and doubled the DRAM traffic through L2 evictions).  The per-source run
+// starts (pidx -> start, per-tile scan, source id) are fetched for all 64
+// sources at once before phase 2 (they were 64 dependent load chains), and
+// TILE_V = 512 keeps the masks at 4 KB per warp (occupancy was limited by
+// shared memory at 24 warps per SM with 1024-vertex tiles).
 constexpr int WP_WARPS = 4;
+constexpr int WP_BLK = TILE_V / 32;          // 32-vertex blocks per tile
+constexpr int WP_LD = WP_BLK + 1;            // padded row of masks (no bank conflicts)
 __global__ void __launch_bounds__(WP_WARPS * 32)
 k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn, uint32_t nw,
               uint32_t nb, uint32_t nseg, const uint32_t *cnt_scan, const uint32_t *cand, const uint32_t *pidx,
               uint64_t b0, const unsigned long long *start, uint64_t jlo, uint32_t *osrc, uint32_t *odst) {
-    __shared__ uint32_t masks_s[WP_WARPS][64 * 32];
+    __shared__ uint32_t masks_s[WP_WARPS][64 * WP_LD];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     uint32_t *masks = masks_s[wl];
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1636,34 +1667,49 @@ k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo
         const uint32_t w = (uint32_t)(task % nw);
         const uint64_t vbeg = (uint64_t)seg * TILE_V, vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
         const int nblk = (int)((vend - vbeg + 31) / 32);
+        // run start and source id of sources 64w + lane and 64w + 32 + lane
+        unsigned long long o_lo = 0, o_hi = 0;
+        uint32_t sid_lo = 0, sid_hi = 0;
+        {
+            const uint32_t i0 = w * 64 + (uint32_t)lane, i1 = i0 + 32;
+            if (i0 < nb) {
+                const uint32_t j = pidx[b0 + i0];
+                o_lo = start[j - jlo] + cnt_scan[(uint64_t)i0 * nseg + seg];
+                sid_lo = cand[j];
+            }
+            if (i1 < nb) {
+                const uint32_t j = pidx[b0 + i1];
+                o_hi = start[j - jlo] + cnt_scan[(uint64_t)i1 * nseg + seg];
+                sid_hi = cand[j];
+            }
+        }
         // (1) masks[b][blk]: which of the 32 vertices of block blk source b reaches
-        for (int blk = 0; blk < 32; ++blk) {
+        for (int blk = 0; blk < WP_BLK; ++blk) {
             const uint64_t vv = vbeg + (uint64_t)blk * 32 + lane;
             const uint64_t x = (blk < nblk && vv < vend) ? ans_word(A, S, Vis, vlo + (uint32_t)vv, w, nw) : 0ull;
             const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+            uint32_t my_lo = 0, my_hi = 0;     // lane b keeps the masks of sources b and b + 32
 #pragma unroll 8
             for (int b = 0; b < 32; ++b) {
                 const unsigned m0 = __ballot_sync(0xffffffffu, (lo >> b) & 1u);
                 const unsigned m1 = __ballot_sync(0xffffffffu, (hi >> b) & 1u);
-                if (lane == 0) {
-                    masks[b * 32 + blk] = m0;
-                    masks[(b + 32) * 32 + blk] = m1;
-                }
+                if (lane == b) { my_lo = m0; my_hi = m1; }
             }
+            masks[lane * WP_LD + blk] = my_lo;
+            masks[(lane + 32) * WP_LD + blk] = my_hi;
         }
         __syncwarp();
-        // (2) per source: walk its 32 block masks in order; each block's
+        // (2) per source: walk its block masks in order; each block's
         // targets go to consecutive positions (a coalesced <= 128 B store),
         // so the source's tile run is written front to back by this warp
+        const uint32_t vb = vlo + (uint32_t)vbeg + (uint32_t)lane;
         for (int b = 0; b < 64; ++b) {
             const uint32_t i = w * 64 + (uint32_t)b;
             if (i >= nb) break;
-            const uint32_t j = pidx[b0 + i];
-            unsigned long long o = start[j - jlo] + cnt_scan[(uint64_t)i * nseg + seg];
-            const uint32_t sid = cand[j];
-            const uint32_t vb = vlo + (uint32_t)vbeg + (uint32_t)lane;
+            unsigned long long o = __shfl_sync(0xffffffffu, b < 32 ? o_lo : o_hi, b & 31);
+            const uint32_t sid = __shfl_sync(0xffffffffu, b < 32 ? sid_lo : sid_hi, b & 31);
             for (int blk = 0; blk < nblk; ++blk) {
-                const uint32_t m = masks[b * 32 + blk];
+                const uint32_t m = masks[b * WP_LD + blk];
                 if (!m) continue;
                 if ((m >> lane) & 1u) {
                     const unsigned long long q = o + __popc(m & lt);
@@ -2854,7 +2900,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             unsigned long long *pe_out = (want_pe && !bounded) ? d_stats + S_PE_POST : nullptr;
             k_count_touched<<<148 * 8, 256, 0, s>>>(A, S, P0, nunits, d_total, dead_final, pe_out);
             if (cn) k_count_total<<<grid_for(cn * 32), 256, 0, s>>>(A, S, Vis, clo, cn, (uint32_t)nw, d_total, ctrl,
-                                                                     nunits, dead_final, pe_out);
+                                                                     nunits, nxwords, dead_final, pe_out);
             ST.kernel_launches += cn ? 2 : 1;
             total += eps_np;
             continue;

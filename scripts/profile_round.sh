@@ -16,10 +16,10 @@ for wl in cfg2 cfg5 cfg3; do
       python scripts/prof_workload.py $wl > $O/traffic_$wl.log 2>&1
 done
 F="--set full --clock-control none --import-source on"
-PROF_NOSTATS=1 ncu $F -k regex:"k_level<" -s 10 -c 1 -o $O/full_k_level_cfg2 python scripts/prof_cfg2.py "a*" > $O/full1.log 2>&1
-PROF_NOSTATS=1 ncu $F -k regex:"k_level<" -s 2 -c 1 -o $O/full_k_level_cfg5 python scripts/prof_workload.py cfg5 > $O/full2.log 2>&1
+PROF_NOSTATS=1 ncu $F -k k_level -s 10 -c 1 -o $O/full_k_level_cfg2 python scripts/prof_cfg2.py "a*" > $O/full1.log 2>&1
+PROF_NOSTATS=1 ncu $F -k k_level -s 2 -c 1 -o $O/full_k_level_cfg5 python scripts/prof_workload.py cfg5 > $O/full2.log 2>&1
 PROF_NOSTATS=1 ncu $F -k regex:k_level_hub -s 2 -c 1 -o $O/full_k_level_hub_cfg5 python scripts/prof_workload.py cfg5 > $O/full3.log 2>&1
 PROF_NOSTATS=1 ncu $F -k regex:k_count_total -c 1 -o $O/full_k_count_total_cfg5 python scripts/prof_workload.py cfg5 > $O/full4.log 2>&1
 PROF_PAIRS=1 ncu $F -k regex:k_write_pairs -c 1 -o $O/full_k_write_pairs_cfg2 python scripts/prof_workload.py cfg2 > $O/full5.log 2>&1
-PROF_NOSTATS=1 ncu $F -k regex:"k_pull<" -s 1 -c 1 -o $O/full_k_pull_cfg3 python scripts/prof_workload.py cfg3 > $O/full6.log 2>&1
+PROF_NOSTATS=1 ncu $F -k k_pull -s 1 -c 1 -o $O/full_k_pull_cfg3 python scripts/prof_workload.py cfg3 > $O/full6.log 2>&1
 echo done
