@@ -1640,11 +1640,13 @@ __global__ void k_fill_eps(unsigned long long *cand_cnt, uint64_t n, unsigned lo
 // Write sorted (src, dst) pairs.  A warp takes one (TILE_V-vertex tile,
 // word) task = 64 sources: (1) ballot transposes give, per source, the masks
 // of the tile's 32-vertex blocks (shared memory); (2) per source, the warp
-// walks its masks in vertex order storing every block's targets
-// contiguously.  Each source's tile run is contiguous (start + per-tile
-// scan), so every output sector is written whole by one warp at one time
-// (per-bit scattered writes across 256 sources kept ~10^6 partial runs open
-// and doubled the DRAM traffic through L2 evictions).  The per-source run
+// expands its tile mask into the run of its targets in shared memory and
+// writes the run with 16-byte vector stores (one (src, dst) pair = 2 x 4 B).
+// Each source's tile run is contiguous (start + per-tile scan), so every
+// output sector is written whole by one warp at one time (per-bit scattered
+// writes across 256 sources kept ~10^6 partial runs open and doubled the DRAM
+// traffic through L2 evictions; a store per 32-vertex block and source cost
+// ~34 instructions per block: 10.8 G per cfg2 launch).  The per-source run
 // starts (pidx -> start, per-tile scan, source id) are fetched for all 64
 // sources at once before phase 2 (they were 64 dependent load chains), and
 // TILE_V = 512 keeps the masks at 4 KB per warp (occupancy was limited by
@@ -1657,11 +1659,11 @@ k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo
               uint32_t nb, uint32_t nseg, const uint32_t *cnt_scan, const uint32_t *cand, const uint32_t *pidx,
               uint64_t b0, const unsigned long long *start, uint64_t jlo, uint32_t *osrc, uint32_t *odst) {
     __shared__ uint32_t masks_s[WP_WARPS][64 * WP_LD];
+    __shared__ __align__(16) uint32_t buf_s[WP_WARPS][TILE_V + 8];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     uint32_t *masks = masks_s[wl];
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
     for (uint64_t task = wid; task < (uint64_t)nseg * nw; task += nwarps) {
         const uint32_t seg = (uint32_t)(task / nw);
         const uint32_t w = (uint32_t)(task % nw);
@@ -1699,25 +1701,59 @@ k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo
             masks[(lane + 32) * WP_LD + blk] = my_hi;
         }
         __syncwarp();
-        // (2) per source: walk its block masks in order; each block's
-        // targets go to consecutive positions (a coalesced <= 128 B store),
-        // so the source's tile run is written front to back by this warp
-        const uint32_t vb = vlo + (uint32_t)vbeg + (uint32_t)lane;
+        // (2) per source b: its TILE_V-bit tile mask -> the run of its targets
+        // staged in shared memory (lane l expands bits [16 l, 16 l + 16) after
+        // a warp scan of the lanes' popcounts), then both columns written with
+        // 16-byte vector stores.  The run is staged at index (o mod 4) so that
+        // the 16-byte-aligned part of the global run maps to aligned shared
+        // vectors (conflict-free LDS.128).
+        uint32_t *buf = buf_s[wl];
+        const bool vec_ok = ((reinterpret_cast<uintptr_t>(osrc) | reinterpret_cast<uintptr_t>(odst)) & 15u) == 0;
+        const uint32_t vb = vlo + (uint32_t)vbeg + (uint32_t)lane * 16u;
         for (int b = 0; b < 64; ++b) {
             const uint32_t i = w * 64 + (uint32_t)b;
             if (i >= nb) break;
-            unsigned long long o = __shfl_sync(0xffffffffu, b < 32 ? o_lo : o_hi, b & 31);
+            const unsigned long long o = __shfl_sync(0xffffffffu, b < 32 ? o_lo : o_hi, b & 31);
             const uint32_t sid = __shfl_sync(0xffffffffu, b < 32 ? sid_lo : sid_hi, b & 31);
-            for (int blk = 0; blk < nblk; ++blk) {
-                const uint32_t m = masks[b * WP_LD + blk];
-                if (!m) continue;
-                if ((m >> lane) & 1u) {
-                    const unsigned long long q = o + __popc(m & lt);
-                    osrc[q] = sid;
-                    odst[q] = vb + (uint32_t)blk * 32u;
-                }
-                o += __popc(m);
+            const int blk = lane >> 1;
+            uint32_t x = blk < nblk ? masks[b * WP_LD + blk] : 0u;
+            x = (lane & 1) ? (x >> 16) : (x & 0xffffu);
+            const uint32_t c = (uint32_t)__popc(x);
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += y;
             }
+            const uint32_t n = __shfl_sync(0xffffffffu, incl, 31);
+            if (n == 0) continue;
+            const uint32_t off = (uint32_t)(o & 3ull);
+            uint32_t pos = off + incl - c;
+            while (x) {
+                const int bt = __ffs(x) - 1;
+                x &= x - 1;
+                buf[pos++] = vb + (uint32_t)bt;
+            }
+            __syncwarp();
+            if (!vec_ok) {                                        // unaligned caller buffers
+                for (uint32_t k = (uint32_t)lane; k < n; k += 32) { osrc[o + k] = sid; odst[o + k] = buf[off + k]; }
+                __syncwarp();
+                continue;
+            }
+            const uint32_t h = min(n, (4u - off) & 3u);          // head up to 16-B alignment
+            if ((uint32_t)lane < h) { osrc[o + lane] = sid; odst[o + lane] = buf[off + lane]; }
+            const uint32_t nvec = (n - h) >> 2;
+            uint4 *vs = reinterpret_cast<uint4 *>(osrc + o + h);
+            uint4 *vd = reinterpret_cast<uint4 *>(odst + o + h);
+            const uint4 *bv = reinterpret_cast<const uint4 *>(buf + (off ? 4u : 0u));
+            const uint4 sv = make_uint4(sid, sid, sid, sid);
+            for (uint32_t k = (uint32_t)lane; k < nvec; k += 32) {
+                vd[k] = bv[k];
+                vs[k] = sv;
+            }
+            const uint32_t t0 = h + 4u * nvec;                    // tail (< 4 elements)
+            if (t0 + (uint32_t)lane < n) { osrc[o + t0 + lane] = sid; odst[o + t0 + lane] = buf[off + t0 + lane]; }
+            __syncwarp();
         }
         __syncwarp();
     }
