@@ -1487,6 +1487,7 @@ __global__ void k_iota(uint32_t *x, uint64_t n) {
 // Ans(v, w) = OR over final states q with v in range_q of Vis[row(q,v), w]:
 // OR-ing the final states deduplicates targets reached in several final
 // states (distinct pairs).
+template <bool L1 = false>
 __device__ __forceinline__ uint64_t ans_word(const DevAuto &A, const Layout &S, const uint64_t *Vis,
                                              uint32_t v, uint64_t w, uint32_t nw) {
     uint64_t acc = 0;
@@ -1494,7 +1495,10 @@ __device__ __forceinline__ uint64_t ans_word(const DevAuto &A, const Layout &S, 
     while (fm) {
         const int q = __ffsll((long long)fm) - 1;
         fm &= fm - 1;
-        if (v - S.lo[q] < S.len[q]) acc |= ld_cg(Vis + (S.row_base[q] + (v - S.lo[q])) * nw + w);
+        if (v - S.lo[q] < S.len[q]) {
+            const uint64_t *p = Vis + (S.row_base[q] + (v - S.lo[q])) * nw + w;
+            acc |= L1 ? __ldg((const unsigned long long *)p) : ld_cg(p);
+        }
     }
     return acc;
 }
@@ -1554,10 +1558,24 @@ __global__ void k_count_total(const DevAuto A, const Layout S, const uint64_t *V
     if (lane == 0 && pacc) atomicAdd(pe, pacc);
 }
 
-// Per-(source, tile) counts by warp ballot transposes: a warp takes a tile of
+// 32 x 32 bit-matrix transpose across a warp: lane i holds row i (bit j =
+// element (i, j)); afterwards lane j holds column j (bit i = element (i, j)).
+// Five rounds swap the off-diagonal s x s blocks (s = 16, 8, 4, 2, 1).
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+    const uint32_t M[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int r = 0; r < 5; ++r) {
+        const int sft = 16 >> r;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, sft);
+        x = (lane & sft) ? ((x & ~M[r]) | ((y & ~M[r]) >> sft)) : ((x & M[r]) | ((y & M[r]) << sft));
+    }
+    return x;
+}
+
+// Per-(source, tile) counts by warp bit transposes: a warp takes a tile of
 // TILE_V vertices and a group of 4 words (32 B = one sector per row); lane l
-// holds vertex v0 + l; ballot over bit b gives the tile's members of source
-// w*64+b.  cnt[(i) * nseg + seg] (u32), i = batch-local source index.
+// holds vertex v0 + l; after the transpose lane b holds the block's members
+// of source w*64+b.  cnt[(i) * nseg + seg] (u32), i = batch-local source index.
 __global__ void k_tile_counts(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
                               uint32_t nw, uint32_t nb, uint32_t nseg, uint32_t *cnt) {
     const int lane = threadIdx.x & 31;
@@ -1578,13 +1596,9 @@ __global__ void k_tile_counts(const DevAuto A, const Layout S, const uint64_t *V
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 if (!__ballot_sync(0xffffffffu, x[k] != 0)) continue;
-                const uint32_t lo = (uint32_t)x[k], hi = (uint32_t)(x[k] >> 32);
-#pragma unroll 8
-                for (int b = 0; b < 32; ++b) {
-                    const unsigned m0 = __ballot_sync(0xffffffffu, (lo >> b) & 1u);
-                    const unsigned m1 = __ballot_sync(0xffffffffu, (hi >> b) & 1u);
-                    if (lane == b) { c[2 * k] += __popc(m0); c[2 * k + 1] += __popc(m1); }
-                }
+                // lane b: the block's members of sources 64 (w0 + k) + b and + 32 + b
+                c[2 * k] += __popc(warp_transpose32((uint32_t)x[k], lane));
+                c[2 * k + 1] += __popc(warp_transpose32((uint32_t)(x[k] >> 32), lane));
             }
         }
 #pragma unroll
@@ -1638,7 +1652,7 @@ __global__ void k_fill_eps(unsigned long long *cand_cnt, uint64_t n, unsigned lo
 }
 
 // Write sorted (src, dst) pairs.  A warp takes one (TILE_V-vertex tile,
-// word) task = 64 sources: (1) ballot transposes give, per source, the masks
+// word) task = 64 sources: (1) warp bit transposes give, per source, the masks
 // of the tile's 32-vertex blocks (shared memory); (2) per source, the warp
 // expands its tile mask into the run of its targets in shared memory and
 // writes the run with 16-byte vector stores (one (src, dst) pair = 2 x 4 B).
@@ -1662,11 +1676,16 @@ k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo
     __shared__ __align__(16) uint32_t buf_s[WP_WARPS][TILE_V + 8];
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
     uint32_t *masks = masks_s[wl];
-    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    for (uint64_t task = wid; task < (uint64_t)nseg * nw; task += nwarps) {
-        const uint32_t seg = (uint32_t)(task / nw);
-        const uint32_t w = (uint32_t)(task % nw);
+    // a CTA takes WP_WARPS consecutive words of one tile (warp wl: word
+    // w4 * WP_WARPS + wl), so the 32-byte sectors of a vertex row are read by
+    // its warps together (L1 hits) instead of by four drifting warps, each of
+    // which missed in an L2 flooded by the output writes (12 GB of reads per
+    // cfg2 launch for 1.15 GB of visited words)
+    const uint64_t nw4 = (nw + WP_WARPS - 1) / WP_WARPS;
+    for (uint64_t ct = blockIdx.x; ct < (uint64_t)nseg * nw4; ct += gridDim.x) {
+      const uint32_t seg = (uint32_t)(ct / nw4);
+      const uint32_t w = (uint32_t)(ct % nw4) * WP_WARPS + (uint32_t)wl;
+      if (w < nw) {
         const uint64_t vbeg = (uint64_t)seg * TILE_V, vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
         const int nblk = (int)((vend - vbeg + 31) / 32);
         // run start and source id of sources 64w + lane and 64w + 32 + lane
@@ -1686,19 +1705,20 @@ k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo
             }
         }
         // (1) masks[b][blk]: which of the 32 vertices of block blk source b reaches
-        for (int blk = 0; blk < WP_BLK; ++blk) {
-            const uint64_t vv = vbeg + (uint64_t)blk * 32 + lane;
-            const uint64_t x = (blk < nblk && vv < vend) ? ans_word(A, S, Vis, vlo + (uint32_t)vv, w, nw) : 0ull;
-            const uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
-            uint32_t my_lo = 0, my_hi = 0;     // lane b keeps the masks of sources b and b + 32
-#pragma unroll 8
-            for (int b = 0; b < 32; ++b) {
-                const unsigned m0 = __ballot_sync(0xffffffffu, (lo >> b) & 1u);
-                const unsigned m1 = __ballot_sync(0xffffffffu, (hi >> b) & 1u);
-                if (lane == b) { my_lo = m0; my_hi = m1; }
+        for (int bk = 0; bk < WP_BLK; bk += 8) {
+            uint64_t xs[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int blk = bk + k;
+                const uint64_t vv = vbeg + (uint64_t)blk * 32 + lane;
+                xs[k] = (blk < nblk && vv < vend) ? ans_word<true>(A, S, Vis, vlo + (uint32_t)vv, w, nw) : 0ull;
             }
-            masks[lane * WP_LD + blk] = my_lo;
-            masks[(lane + 32) * WP_LD + blk] = my_hi;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                // lane b keeps the masks of sources b and b + 32
+                masks[lane * WP_LD + bk + k] = warp_transpose32((uint32_t)xs[k], lane);
+                masks[(lane + 32) * WP_LD + bk + k] = warp_transpose32((uint32_t)(xs[k] >> 32), lane);
+            }
         }
         __syncwarp();
         // (2) per source b: its TILE_V-bit tile mask -> the run of its targets
@@ -1729,11 +1749,9 @@ k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo
             if (n == 0) continue;
             const uint32_t off = (uint32_t)(o & 3ull);
             uint32_t pos = off + incl - c;
-            while (x) {
-                const int bt = __ffs(x) - 1;
-                x &= x - 1;
-                buf[pos++] = vb + (uint32_t)bt;
-            }
+#pragma unroll
+            for (int bt = 0; bt < 16; ++bt)
+                if ((x >> bt) & 1u) buf[pos++] = vb + (uint32_t)bt;
             __syncwarp();
             if (!vec_ok) {                                        // unaligned caller buffers
                 for (uint32_t k = (uint32_t)lane; k < n; k += 32) { osrc[o + k] = sid; odst[o + k] = buf[off + k]; }
@@ -1755,7 +1773,8 @@ k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo
             if (t0 + (uint32_t)lane < n) { osrc[o + t0 + lane] = sid; odst[o + t0 + lane] = buf[off + t0 + lane]; }
             __syncwarp();
         }
-        __syncwarp();
+      }
+      __syncthreads();
     }
 }
 
