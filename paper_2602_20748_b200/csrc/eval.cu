@@ -173,6 +173,7 @@ struct LevelArgs {
     uint64_t *ActCur, *ActNext;
     uint64_t total_units;      // work units of the whole state (direction heuristic)
     uint32_t pull_mode;        // 0: top-down only; 1: bottom-up on dense levels
+    uint32_t tma;              // 1: k_level<.., TMA = true> (bulk-copy expand ring)
 };
 
 // stats slots
@@ -497,6 +498,131 @@ __device__ __forceinline__ void flush_stats(unsigned long long *st, unsigned lon
     }
 }
 
+// ---- TMA bulk-copy expand (sm_100a): the target-row segments of a row's
+// edges are fetched by cp.async.bulk into a per-warp shared-memory ring
+// (TMA_NS slots of up to KGRP chunks x 256 B), completion on an mbarrier per
+// slot.  With KC = 8 active chunks the register path holds one edge's 8 words
+// per lane in flight (a row with d edges costs d DRAM round trips); the ring
+// keeps TMA_NS edges in flight without registers.
+#ifndef RPQ_TMA_NS
+#define RPQ_TMA_NS 4
+#endif
+constexpr int TMA_NS = RPQ_TMA_NS;
+#ifndef RPQ_TMA_MINB
+#define RPQ_TMA_MINB 3
+#endif
+constexpr uint32_t TMA_SLOT = KGRP * 32 * 8;          // bytes per slot (8 chunks of 32 words)
+constexpr int TMA_WARPS = 8;
+constexpr uint32_t TMA_WARP_BYTES = TMA_NS * TMA_SLOT + 64;
+constexpr uint32_t TMA_SMEM = TMA_WARPS * TMA_WARP_BYTES;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n selp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+struct TmaRing {
+    uint64_t *buf;     // TMA_NS slots of TMA_SLOT bytes
+    uint64_t *bar;     // TMA_NS mbarriers
+    uint32_t phase;    // bit s = parity to wait for on slot s
+};
+
+// Same contract as expand_edges for a group whose nk active chunks lie in a
+// window of <= KGRP chunks starting at chunk c0 (bits relative to the X word).
+template <bool STATS>
+__device__ __forceinline__ void expand_edges_tma(const LevelArgs &p, const Layout &S, uint32_t q2,
+                                                 const uint32_t *__restrict__ nbr, uint32_t beg, uint32_t end,
+                                                 const uint64_t (&f)[KGRP], uint64_t bits, int nk, uint32_t c0,
+                                                 uint32_t span, uint32_t xw, int lane, unsigned long long *st,
+                                                 bool &act, bool live, TmaRing &R) {
+    const uint32_t tbase = (uint32_t)(S.row_base[q2] - S.lo[q2]);
+    const uint32_t colw = (xw * 32u + c0) * 32u;            // first word of the window (cw == 32)
+    const uint32_t bytes = span * 256u;
+    int fpop = 0, nzw = 0;
+#pragma unroll
+    for (int k = 0; k < KGRP; ++k) { fpop += __popcll(f[k]); nzw += f[k] != 0; }
+    for (uint32_t j = beg; j < end; j += 32) {
+        const uint32_t my = (j + lane < end) ? __ldg(nbr + j + lane) : 0u;
+        const int cnt = (int)((end - j) < 32u ? (end - j) : 32u);
+        auto issue = [&](int e) {
+            const int sl = e % TMA_NS;
+            const uint32_t trow = tbase + __shfl_sync(0xffffffffu, my, e & 31);
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(R.bar + sl, bytes);
+                bulk_g2s(R.buf + (size_t)sl * (TMA_SLOT / 8), p.Vis + (uint64_t)trow * p.nw + colw, bytes, R.bar + sl);
+            }
+            return trow;
+        };
+        uint32_t trows[TMA_NS];
+#pragma unroll
+        for (int e = 0; e < TMA_NS; ++e)
+            if (e < cnt) trows[e] = issue(e);
+        for (int e = 0; e < cnt; ++e) {
+            const int sl = e % TMA_NS;
+            while (!mbar_try(R.bar + sl, (R.phase >> sl) & 1u)) {
+            }
+            R.phase ^= 1u << sl;
+            uint32_t trow = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < TMA_NS; ++s2)
+                if (s2 == sl) trow = trows[s2];
+            const uint64_t *sb = R.buf + (size_t)sl * (TMA_SLOT / 8);
+            const uint64_t rb = (uint64_t)trow * p.nw + colw + lane;
+            uint32_t lm = 0;
+#pragma unroll
+            for (int k = 0; k < KGRP; ++k) {
+                if (k >= nk) break;
+                const uint32_t ck = ((uint32_t)(bits >> (8 * k)) & 0xffu) - c0;
+                const uint64_t m = f[k] & ~sb[ck * 32u + lane];
+                if (m) {
+                    red_or64(p.Vis + rb + ck * 32u, m);
+                    lm |= 1u << (ck + c0);
+                    if (STATS) st[S_N_RED]++;
+                }
+            }
+            const uint32_t newmask = live ? __reduce_or_sync(0xffffffffu, lm) : 0u;
+            if (lane == 0 && newmask) {
+                const uint64_t xi = (uint64_t)trow * p.nxw + xw;
+                red_or32(p.Xnext + xi, newmask);
+                red_or32(p.XBnext + (xi >> 10), 1u << ((xi >> 5) & 31));
+                act = true;
+                if (STATS) st[S_X_RED]++;
+            }
+            __syncwarp();                     // every lane has read the slot
+            if (e + TMA_NS < cnt) {
+                const uint32_t tr = issue(e + TMA_NS);
+#pragma unroll
+                for (int s2 = 0; s2 < TMA_NS; ++s2)
+                    if (s2 == sl) trows[s2] = tr;
+            }
+        }
+        if (STATS && nzw) {
+            st[S_WORD_EDGE] += (unsigned long long)nzw * cnt;
+            st[S_PE] += (unsigned long long)fpop * cnt;
+        }
+        if (STATS && lane == 0) st[S_ITEM_EDGES] += cnt;
+    }
+}
+
 template <bool STATS, bool BND = false>
 __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const Layout &S, uint32_t q2,
                                                const uint32_t *nbr, uint32_t beg, uint32_t end,
@@ -518,16 +644,28 @@ __device__ __forceinline__ void dispatch_edges(int nk, const LevelArgs &p, const
 // f = Vis & ~Done; Done |= f) and then expanded along every automaton
 // transition of the row's state.  Work units (32 X words = one XB bit) are
 // interleaved over warps.
-template <bool STATS, bool BND = false>
-__global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, const Layout *__restrict__ Sg,
-                                                               const LevelArgs p) {
+template <bool STATS, bool BND = false, bool TMA = false>
+__global__ void __launch_bounds__(256, TMA ? RPQ_TMA_MINB : RPQ_LEVEL_MINB) k_level(const DevAuto A, const Layout *__restrict__ Sg,
+                                                                         const LevelArgs p) {
     if (level_pull(p)) return;                 // bottom-up level: k_pull_prep + k_pull
     if (BND && *(volatile const uint32_t *)&p.ctrl->blevel > p.level_lim) return;   // length bound reached
     __shared__ Layout S;
-    __shared__ unsigned long long actS[ACT_SMEM_WORDS];
+    __shared__ unsigned long long actS[TMA ? 1 : ACT_SMEM_WORDS];
+    extern __shared__ __align__(128) unsigned char tma_dyn[];
     load_layout(S, Sg, A.nq);
-    if (p.pull_mode) act_init(actS, p.nw);
+    if (!TMA && p.pull_mode) act_init(actS, p.nw);
     const int lane = threadIdx.x & 31;
+    TmaRing ring{};
+    if constexpr (TMA) {
+        unsigned char *wb = tma_dyn + (threadIdx.x >> 5) * TMA_WARP_BYTES;
+        ring.bar = reinterpret_cast<uint64_t *>(wb);
+        ring.buf = reinterpret_cast<uint64_t *>(wb + 64);
+        if (lane == 0) {
+            for (int sl = 0; sl < TMA_NS; ++sl) mbar_init(ring.bar + sl, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
     const uint32_t nunits = *(volatile uint32_t *)&p.ctrl->ucnt[p.par];
@@ -609,7 +747,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                     if (f[k]) {
                         (BND ? p.Mark : p.Done)[rb + bt * p.cw] = dd[k] | f[k];
                         // sources of this frontier word may gain bits next level
-                        if (p.pull_mode) act_or(actS, p.ActNext, (uint32_t)(rb - row * p.nw) + bt * p.cw, f[k]);
+                        if (!TMA && p.pull_mode) act_or(actS, p.ActNext, (uint32_t)(rb - row * p.nw) + bt * p.cw, f[k]);
                         if (STATS) st[S_WORD_ITEMS]++;
                     }
                 }
@@ -673,6 +811,17 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
                                 p.hrecs[r + sg] = HubRec{0u, 0u, 0u, 0u};
                         }
                     }
+                    if constexpr (TMA) {
+                        // chunk window of the group (bits ascend: chunk of k = 0 is the first)
+                        const uint32_t c0 = (uint32_t)bits & 0xffu;
+                        const uint32_t cl = (uint32_t)(bits >> (8 * (nk - 1))) & 0xffu;
+                        const uint32_t span = cl - c0 + 1u;
+                        if (nk >= 2 && span <= (uint32_t)KGRP && (xw * 32u + c0 + span) * 32u <= p.nw) {
+                            expand_edges_tma<STATS>(p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, nk, c0, span, xw,
+                                                    lane, st, act, A.toff[A.tto[t] + 1] > A.toff[A.tto[t]], ring);
+                            continue;
+                        }
+                    }
                     dispatch_edges<STATS, BND>(nk, p, S, A.tto[t], A.nbr[slot], beg, end, f, bits, xw, lane, st, act,
                                           A.toff[A.tto[t] + 1] > A.toff[A.tto[t]]);
                 }
@@ -681,7 +830,7 @@ __global__ void __launch_bounds__(256, RPQ_LEVEL_MINB) k_level(const DevAuto A, 
     }
     if (__ballot_sync(0xffffffffu, act) && lane == 0) p.ctrl->active[p.par ^ 1] = 1u;
     flush_stats<STATS>(st, p.stats);
-    if (p.pull_mode) act_flush(actS, p.ActNext, p.nw);
+    if (!TMA && p.pull_mode) act_flush(actS, p.ActNext, p.nw);
 }
 
 // Deferred long rows: a warp per HUB_EDGES-edge segment.
@@ -1928,12 +2077,12 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
     if ((e = cudaGraphAddNode(&cn, LG.g, nullptr, 0, &cp)) != cudaSuccess) return e;
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     cudaGraphNode_t prev = nullptr;
-    auto add = [&](void *fn, dim3 gr, dim3 bl, void **args) -> cudaError_t {
+    auto add = [&](void *fn, dim3 gr, dim3 bl, void **args, unsigned smem = 0) -> cudaError_t {
         cudaKernelNodeParams kp{};
         kp.func = fn;
         kp.gridDim = gr;
         kp.blockDim = bl;
-        kp.sharedMemBytes = 0;
+        kp.sharedMemBytes = smem;
         kp.kernelParams = args;
         cudaGraphNode_t n;
         cudaError_t r = cudaGraphAddKernelNode(&n, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp);
@@ -1956,12 +2105,15 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
     const bool pull = P0.pull_mode != 0;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u0)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r0)) != cudaSuccess) return e;
-    if ((e = add((void *)k_level<STATS, BND>, dim3(grid), dim3(256), a0)) != cudaSuccess) return e;
+    void *lvl = P0.tma ? (void *)k_level<STATS, false, true> : (void *)k_level<STATS, BND>;
+    const int lgr = P0.tma ? 148 * RPQ_TMA_MINB : grid;
+    const unsigned lsm = P0.tma ? TMA_SMEM : 0u;
+    if ((e = add(lvl, dim3(lgr), dim3(256), a0, lsm)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a0)) != cudaSuccess) return e;
     if (hub && (e = add((void *)k_level_hub<STATS, BND>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u1)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r1)) != cudaSuccess) return e;
-    if ((e = add((void *)k_level<STATS, BND>, dim3(grid), dim3(256), a1)) != cudaSuccess) return e;
+    if ((e = add(lvl, dim3(lgr), dim3(256), a1, lsm)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a1)) != cudaSuccess) return e;
     if (hub && (e = add((void *)k_level_hub<STATS, BND>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_end, dim3(1), dim3(1), m1)) != cudaSuccess) return e;
@@ -1981,12 +2133,14 @@ rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &
         if (P.pull_mode) k_pull_prep<<<148 * 8, 256, 0, s>>>(A, P);
         if (stats) {
             if (P.bounded) k_level<true, true><<<grid, 256, 0, s>>>(A, Sg, P);
+            else if (P.tma) k_level<true, false, true><<<148 * RPQ_TMA_MINB, 256, TMA_SMEM, s>>>(A, Sg, P);
             else k_level<true><<<grid, 256, 0, s>>>(A, Sg, P);
             if (P.pull_mode) k_pull<true><<<148 * 8, 256, 0, s>>>(A, Sg, P);
             if (hub && P.bounded) k_level_hub<true, true><<<hgrid, 256, 0, s>>>(A, Sg, P);
             else if (hub) k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
         } else {
             if (P.bounded) k_level<false, true><<<grid, 256, 0, s>>>(A, Sg, P);
+            else if (P.tma) k_level<false, false, true><<<148 * RPQ_TMA_MINB, 256, TMA_SMEM, s>>>(A, Sg, P);
             else k_level<false><<<grid, 256, 0, s>>>(A, Sg, P);
             if (P.pull_mode) k_pull<false><<<148 * 8, 256, 0, s>>>(A, Sg, P);
             if (hub && P.bounded) k_level_hub<false, true><<<hgrid, 256, 0, s>>>(A, Sg, P);
@@ -2718,6 +2872,20 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         P0.ActNext = Act ? Act + nw : nullptr;
     }
     P0.bounded = bounded ? 1u : 0u;
+    {   // bulk-copy (TMA) expand: RPQ_TMA=1 (needs 32-word chunks; not with bounded or pull levels)
+        const char *et = getenv("RPQ_TMA");
+        P0.tma = (et && et[0] == '1' && !bounded && !P0.pull_mode && CW == 32) ? 1u : 0u;
+        if (P0.tma) {
+            static bool attr_set = false;
+            if (!attr_set) {
+                cudaFuncSetAttribute((const void *)k_level<false, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
+                cudaFuncSetAttribute((const void *)k_level<true, false, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
+                attr_set = true;
+            }
+        }
+    }
     // levels (ctrl->levels, counted from 1) that may expand: level L performs
     // hop L, or hop L + 1 when the seeds were expanded by k_seed_expand
     P0.level_lim = !bounded ? ~0u : skip_q0 ? (max_hops ? max_hops - 1 : 0) : max_hops;

@@ -1,10 +1,7 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_stream.py tests/test_gpu_dist.py tests/test_gpu_targets.py tests/test_gpu_crpq.py "tests/test_gpu_exact.py::test_cfg2_pairs_of_2048_sources" -q -x > gpurun_out/it_t.log 2>&1
-tail -3 gpurun_out/it_t.log
-timeout 600 python bench.py --steps 5 --warmup 3 --no-north-star --no-cfg3 --no-cpu-baseline > gpurun_out/it_b.json 2> gpurun_out/it_b.err
-python -c "import json; d=json.loads(open('gpurun_out/it_b.json').read().splitlines()[-1]); print(d['ms_per_step'], d['roofline']['frac'], d['pairs_mode'])"
-O=gpurun_out/pairsprof; mkdir -p $O
-export RPQ_HOST_LOOP=1
-PROF_PAIRS=1 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none -k regex:"k_write_pairs|k_tile_counts" --csv --log-file $O/launches_pairs_v4.csv python scripts/prof_workload.py cfg2 > $O/l.log 2>&1
-grep -h k_write_pairs $O/launches_pairs_v4.csv | head -12 | cut -c1-60,200-
+rm -f gpurun_out/it_tv.log
+for wl in cfg2 "rmat24 64"; do
+  for v in t2m5 t3m4 t6m2 t8m1; do RPQ_TMA=1 RPQ_LIB_PATH=build/variants/librpq_$v.so timeout 600 python scripts/time_variant.py $wl >> gpurun_out/it_tv.log 2>&1; done
+done
+cut -c1-100 gpurun_out/it_tv.log

@@ -339,3 +339,20 @@ def test_sparse_batches_dense_engine(monkeypatch):
             assert gpu_eval(G, rx, R.RPQ_COUNT, batch_sources=B).count == want.shape[0], (rx, B)
         r = gpu_eval(G, rx, R.RPQ_PAIRS, batch_sources=128)
         assert_pairs_equal(r.rows(), want, rx)
+
+
+@pytest.mark.parametrize("B", [0, 4096])
+def test_tma_bulk_copy_expand(B, monkeypatch):
+    """RPQ_TMA=1: the target-row segments of KC >= 2 chunk groups arrive by
+    cp.async.bulk into a per-warp shared-memory ring (mbarrier completion);
+    pairs and PE must equal the oracle's (multi-chunk rows: B = 0 puts all
+    20 K sources in one batch, 10 chunks per row)."""
+    monkeypatch.setenv("RPQ_TMA", "1")
+    monkeypatch.setenv("RPQ_ENGINE", "dense")
+    g = synth.random_graph(20000, 70000, 3, seed=12)
+    G = R.rpq_graph_load(g)
+    for rx in ["a*", "(a|b)*c", "a b* c"]:
+        want, o = oracle_rows(g, rx)
+        r = gpu_eval(G, rx, R.RPQ_PAIRS | R.RPQ_STATS, batch_sources=B)
+        assert_pairs_equal(r.rows(), want, (rx, B))
+        assert r.stats()["product_edges"] == int(o["pe"].sum()), rx
