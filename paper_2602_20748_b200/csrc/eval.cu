@@ -2072,28 +2072,39 @@ Range hull(Range a, Range b) {
 struct LevelGraph {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t exec = nullptr;
+    cudaGraphConditionalHandle h{};
+    std::vector<cudaGraphNode_t> nodes;   // body kernel nodes, in build order
     ~LevelGraph() {
         if (exec) cudaGraphExecDestroy(exec);
         if (g) cudaGraphDestroy(g);
     }
 };
 
+// update = true: LG holds an instantiated graph of the same topology (same
+// kernels and node order); only the kernel arguments and grids are patched
+// into its body nodes (cudaGraphExecKernelNodeSetParams, microseconds)
+// instead of a new instantiation (~0.3 ms on a cold query, e.g. a new graph).
 template <bool STATS, bool BND>
 cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg, const LevelArgs &P0,
-                              const LevelArgs &P1, int grid, int hgrid, uint64_t nxbwords, bool hub) {
+                              const LevelArgs &P1, int grid, int hgrid, uint64_t nxbwords, bool hub,
+                              bool update = false) {
     cudaError_t e;
-    if ((e = cudaGraphCreate(&LG.g, 0)) != cudaSuccess) return e;
-    cudaGraphConditionalHandle h;
-    if ((e = cudaGraphConditionalHandleCreate(&h, LG.g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) return e;
-    cudaGraphNodeParams cp{};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t cn;
-    if ((e = cudaGraphAddNode(&cn, LG.g, nullptr, 0, &cp)) != cudaSuccess) return e;
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraph_t body = nullptr;
+    if (!update) {
+        if ((e = cudaGraphCreate(&LG.g, 0)) != cudaSuccess) return e;
+        if ((e = cudaGraphConditionalHandleCreate(&LG.h, LG.g, 1, cudaGraphCondAssignDefault)) != cudaSuccess) return e;
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = LG.h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t cn;
+        if ((e = cudaGraphAddNode(&cn, LG.g, nullptr, 0, &cp)) != cudaSuccess) return e;
+        body = cp.conditional.phGraph_out[0];
+        LG.nodes.clear();
+    }
     cudaGraphNode_t prev = nullptr;
+    size_t ni = 0;
     auto add = [&](void *fn, dim3 gr, dim3 bl, void **args, unsigned smem = 0) -> cudaError_t {
         cudaKernelNodeParams kp{};
         kp.func = fn;
@@ -2101,11 +2112,17 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
         kp.blockDim = bl;
         kp.sharedMemBytes = smem;
         kp.kernelParams = args;
+        if (update) {
+            if (ni >= LG.nodes.size()) return cudaErrorInvalidValue;
+            return cudaGraphExecKernelNodeSetParams(LG.exec, LG.nodes[ni++], &kp);
+        }
         cudaGraphNode_t n;
         cudaError_t r = cudaGraphAddKernelNode(&n, body, prev ? &prev : nullptr, prev ? 1 : 0, &kp);
         prev = n;
+        LG.nodes.push_back(n);
         return r;
     };
+    cudaGraphConditionalHandle h = LG.h;
     DevAuto a = A;
     const Layout *sg = Sg;
     LevelArgs p0 = P0, p1 = P1;
@@ -2134,6 +2151,7 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a1)) != cudaSuccess) return e;
     if (hub && (e = add((void *)k_level_hub<STATS, BND>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_end, dim3(1), dim3(1), m1)) != cudaSuccess) return e;
+    if (update) return ni == LG.nodes.size() ? cudaSuccess : cudaErrorInvalidValue;
     return cudaGraphInstantiate(&LG.exec, LG.g, 0);
 }
 
@@ -2559,22 +2577,30 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             }
             if (cached >= 0) use = cached != 0;
             if (!use && cached < 0) {
-                const uint64_t ns = std::min<uint64_t>(np, 2048);
-                uint32_t *didx = (uint32_t *)ws.get(ns * 4);
-                if (!didx) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
-                k_sample_idx<<<grid_for(ns), 256, 0, s>>>(didx, ns, np);   // k * np / ns, evenly spread
-                k_sparse<false, false><<<grid_for(ns * 32, SP_WARPS * 32, 148 * 8), SP_WARPS * 32, 0, s>>>(
-                    A, cand, pidx, didx, ns, B, 0, 1, sc, sov, d_stats);
-                // overflow flags of the sampled indices, summed on the device
+                // two stages: 256 evenly spread sources settle clearly dense
+                // queries (>= 25 % overflow; the warp tier's 1,024-key probe
+                // of 2,048 sources cost ~0.3 ms per cold query), otherwise
+                // 2,048 sources decide (<= 2 % overflow -> sparse engine)
                 unsigned long long *d_nov = (unsigned long long *)ws.get(8);
                 if (!d_nov) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
-                k_sum_flags<<<1, 256, 0, s>>>(sov, didx, ns, d_nov);
-                ST.kernel_launches += 2;
-                unsigned long long nov = 0;
-                RPQ_CUDA_TRY(cudaMemcpyAsync(&nov, d_nov, 8, cudaMemcpyDeviceToHost, s));
-                RPQ_CUDA_TRY(cudaStreamSynchronize(s));
-                HM("sparse sample");
-                use = nov * 50 <= ns;   // <= 2 % of the sample overflows
+                const uint64_t stage_ns[2] = {std::min<uint64_t>(np, 256), std::min<uint64_t>(np, 2048)};
+                for (int stage = 0; stage < 2; ++stage) {
+                    const uint64_t ns = stage_ns[stage];
+                    uint32_t *didx = (uint32_t *)ws.get(ns * 4);
+                    if (!didx) return fail(rpq_fail(RPQ_ENOMEM, "oom"));
+                    k_sample_idx<<<grid_for(ns), 256, 0, s>>>(didx, ns, np);   // k * np / ns, evenly spread
+                    k_sparse<false, false><<<grid_for(ns * 32, SP_WARPS * 32, 148 * 8), SP_WARPS * 32, 0, s>>>(
+                        A, cand, pidx, didx, ns, B, 0, 1, sc, sov, d_stats);
+                    // overflow flags of the sampled indices, summed on the device
+                    k_sum_flags<<<1, 256, 0, s>>>(sov, didx, ns, d_nov);
+                    ST.kernel_launches += 3;
+                    unsigned long long nov = 0;
+                    RPQ_CUDA_TRY(cudaMemcpyAsync(&nov, d_nov, 8, cudaMemcpyDeviceToHost, s));
+                    RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                    HM("sparse sample");
+                    use = nov * 50 <= ns;
+                    if (stage == 0 && (nov * 4 >= ns || ns == stage_ns[1])) break;
+                }
                 if (allpairs) {
                     std::lock_guard<std::mutex> lk(g->plan_mu);
                     g->engine_cache.emplace_back(sig, use ? 1 : 0);
@@ -2921,7 +2947,8 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     // stream-ordered pool handing back the same blocks -- the same state
     // buffers); otherwise it is rebuilt.  Saves the ~0.1 ms instantiate.
     struct CachedGraph {
-        std::vector<unsigned char> key;
+        std::vector<unsigned char> key;    // every kernel argument
+        std::vector<int> topo;             // kernels / node order
         std::unique_ptr<LevelGraph> lg;
     };
     // (heap object, never destroyed: no graph teardown after the CUDA runtime
@@ -2944,9 +2971,27 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         put(&d_layout, sizeof(d_layout));
         put(&P0, sizeof(P0));
         put(&P1, sizeof(P1));
+        const std::vector<int> topo = {dev, lgrid, hgrid, need_hub ? 1 : 0, stats ? 1 : 0, bounded ? 1 : 0,
+                                       (int)P0.pull_mode, (int)P0.tma};
+        bool updated = false;
         if (cache.lg && cache.lg->exec && cache.key == key) {
             LGp = cache.lg.get();
-        } else {
+        } else if (cache.lg && cache.lg->exec && cache.topo == topo) {
+            // same kernels, new arguments (another graph / state buffers): patch the nodes
+            cudaError_t ue =
+                stats ? (bounded ? build_level_graph<true, true>(*cache.lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub, true)
+                                 : build_level_graph<true, false>(*cache.lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub, true))
+                      : (bounded ? build_level_graph<false, true>(*cache.lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub, true)
+                                 : build_level_graph<false, false>(*cache.lg, A, d_layout, P0, P1, lgrid, hgrid, xbwords, need_hub, true));
+            if (ue == cudaSuccess) {
+                cache.key = std::move(key);
+                LGp = cache.lg.get();
+                updated = true;
+            } else {
+                cudaGetLastError();
+            }
+        }
+        if (LGp == &local && !updated) {
             cache.lg.reset();
             auto lg = std::make_unique<LevelGraph>();
             cudaError_t ge =
@@ -2960,6 +3005,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                 lg->exec = nullptr;
             } else {
                 cache.key = std::move(key);
+                cache.topo = topo;
                 cache.lg = std::move(lg);
                 LGp = cache.lg.get();
             }

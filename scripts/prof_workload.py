@@ -18,7 +18,7 @@ for rx in bench.WORKLOADS[wl]["queries"]:
     mode = R.RPQ_COUNT if os.environ.get("PROF_NOSTATS") else R.RPQ_COUNT | R.RPQ_STATS
     if os.environ.get("PROF_PAIRS"):
         mode = R.RPQ_PAIRS
-    B = R.rpq_plan(G, a, stream=s)["batch_sources"] if shards > 1 else 0
+    B = R.rpq_plan(G, a, stream=s, shard_count=shards)["batch_sources"] if shards > 1 else 0
     r = R.rpq_eval_allpairs(G, a, mode=mode, stream=s, shard_index=0, shard_count=shards, batch_sources=B)
     torch.cuda.synchronize()
     st = r.stats()
