@@ -564,6 +564,9 @@ struct TmaRing {
 
 // Same contract as expand_edges for a group whose nk active chunks lie in a
 // window of <= KGRP chunks starting at chunk c0 (bits relative to the X word).
+// The ring runs over the whole edge range [beg, end) (hub segments: up to 512
+// edges), with the neighbour ids of the current and the next 32-edge window
+// held in registers, so it never drains at window boundaries.
 template <bool STATS>
 __device__ __forceinline__ void expand_edges_tma(const LevelArgs &p, const Layout &S, uint32_t q2,
                                                  const uint32_t *__restrict__ nbr, uint32_t beg, uint32_t end,
@@ -573,71 +576,70 @@ __device__ __forceinline__ void expand_edges_tma(const LevelArgs &p, const Layou
     const uint32_t tbase = (uint32_t)(S.row_base[q2] - S.lo[q2]);
     const uint32_t colw = (xw * 32u + c0) * 32u;            // first word of the window (cw == 32)
     const uint32_t bytes = span * 256u;
-    int fpop = 0, nzw = 0;
-#pragma unroll
-    for (int k = 0; k < KGRP; ++k) { fpop += __popcll(f[k]); nzw += f[k] != 0; }
-    for (uint32_t j = beg; j < end; j += 32) {
-        const uint32_t my = (j + lane < end) ? __ldg(nbr + j + lane) : 0u;
-        const int cnt = (int)((end - j) < 32u ? (end - j) : 32u);
-        auto issue = [&](int e) {
-            const int sl = e % TMA_NS;
-            const uint32_t trow = tbase + __shfl_sync(0xffffffffu, my, e & 31);
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(R.bar + sl, bytes);
-                bulk_g2s(R.buf + (size_t)sl * (TMA_SLOT / 8), p.Vis + (uint64_t)trow * p.nw + colw, bytes, R.bar + sl);
-            }
-            return trow;
-        };
-        uint32_t trows[TMA_NS];
-#pragma unroll
-        for (int e = 0; e < TMA_NS; ++e)
-            if (e < cnt) trows[e] = issue(e);
-        for (int e = 0; e < cnt; ++e) {
-            const int sl = e % TMA_NS;
-            while (!mbar_try(R.bar + sl, (R.phase >> sl) & 1u)) {
-            }
-            R.phase ^= 1u << sl;
-            uint32_t trow = 0;
-#pragma unroll
-            for (int s2 = 0; s2 < TMA_NS; ++s2)
-                if (s2 == sl) trow = trows[s2];
-            const uint64_t *sb = R.buf + (size_t)sl * (TMA_SLOT / 8);
-            const uint64_t rb = (uint64_t)trow * p.nw + colw + lane;
-            uint32_t lm = 0;
-#pragma unroll
-            for (int k = 0; k < KGRP; ++k) {
-                if (k >= nk) break;
-                const uint32_t ck = ((uint32_t)(bits >> (8 * k)) & 0xffu) - c0;
-                const uint64_t m = f[k] & ~sb[ck * 32u + lane];
-                if (m) {
-                    red_or64(p.Vis + rb + ck * 32u, m);
-                    lm |= 1u << (ck + c0);
-                    if (STATS) st[S_N_RED]++;
-                }
-            }
-            const uint32_t newmask = live ? __reduce_or_sync(0xffffffffu, lm) : 0u;
-            if (lane == 0 && newmask) {
-                const uint64_t xi = (uint64_t)trow * p.nxw + xw;
-                red_or32(p.Xnext + xi, newmask);
-                red_or32(p.XBnext + (xi >> 10), 1u << ((xi >> 5) & 31));
-                act = true;
-                if (STATS) st[S_X_RED]++;
-            }
-            __syncwarp();                     // every lane has read the slot
-            if (e + TMA_NS < cnt) {
-                const uint32_t tr = issue(e + TMA_NS);
-#pragma unroll
-                for (int s2 = 0; s2 < TMA_NS; ++s2)
-                    if (s2 == sl) trows[s2] = tr;
-            }
+    if (beg >= end) return;
+    uint32_t wbase = beg;
+    uint32_t my_cur = (beg + lane < end) ? __ldg(nbr + beg + lane) : 0u;
+    uint32_t my_nxt = (beg + 32 + lane < end) ? __ldg(nbr + beg + 32 + lane) : 0u;
+    uint32_t trows[TMA_NS];
+    auto issue = [&](uint32_t e) {   // edge e (absolute), e - wbase < 64
+        const uint32_t d = e - wbase;
+        const uint32_t a = __shfl_sync(0xffffffffu, my_cur, d & 31);
+        const uint32_t b2 = __shfl_sync(0xffffffffu, my_nxt, d & 31);
+        const uint32_t trow = tbase + (d < 32 ? a : b2);
+        const int sl = (int)((e - beg) % TMA_NS);
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(R.bar + sl, bytes);
+            bulk_g2s(R.buf + (size_t)sl * (TMA_SLOT / 8), p.Vis + (uint64_t)trow * p.nw + colw, bytes, R.bar + sl);
         }
-        if (STATS && nzw) {
-            st[S_WORD_EDGE] += (unsigned long long)nzw * cnt;
-            st[S_PE] += (unsigned long long)fpop * cnt;
+#pragma unroll
+        for (int s2 = 0; s2 < TMA_NS; ++s2)
+            if (s2 == sl) trows[s2] = trow;
+    };
+    for (uint32_t e = beg; e < end && e < beg + TMA_NS; ++e) issue(e);
+    for (uint32_t e = beg; e < end; ++e) {
+        if (e == wbase + 32) {               // next window of neighbour ids
+            wbase += 32;
+            my_cur = my_nxt;
+            my_nxt = (wbase + 32 + lane < end) ? __ldg(nbr + wbase + 32 + lane) : 0u;
         }
-        if (STATS && lane == 0) st[S_ITEM_EDGES] += cnt;
+        const int sl = (int)((e - beg) % TMA_NS);
+        while (!mbar_try(R.bar + sl, (R.phase >> sl) & 1u)) {
+        }
+        R.phase ^= 1u << sl;
+        uint32_t trow = 0;
+#pragma unroll
+        for (int s2 = 0; s2 < TMA_NS; ++s2)
+            if (s2 == sl) trow = trows[s2];
+        const uint64_t *sb = R.buf + (size_t)sl * (TMA_SLOT / 8);
+        const uint64_t rb = (uint64_t)trow * p.nw + colw + lane;
+        uint32_t lm = 0;
+        int nzw = 0, fpop = 0;
+#pragma unroll
+        for (int k = 0; k < KGRP; ++k) {
+            if (k >= nk) break;
+            const uint32_t ck = ((uint32_t)(bits >> (8 * k)) & 0xffu) - c0;
+            const uint64_t m = f[k] & ~sb[ck * 32u + lane];
+            if (m) {
+                red_or64(p.Vis + rb + ck * 32u, m);
+                lm |= 1u << (ck + c0);
+                if (STATS) st[S_N_RED]++;
+            }
+            if (STATS) { nzw += f[k] != 0; fpop += __popcll(f[k]); }
+        }
+        if (STATS) { st[S_WORD_EDGE] += nzw; st[S_PE] += fpop; }
+        const uint32_t newmask = live ? __reduce_or_sync(0xffffffffu, lm) : 0u;
+        if (lane == 0 && newmask) {
+            const uint64_t xi = (uint64_t)trow * p.nxw + xw;
+            red_or32(p.Xnext + xi, newmask);
+            red_or32(p.XBnext + (xi >> 10), 1u << ((xi >> 5) & 31));
+            act = true;
+            if (STATS) st[S_X_RED]++;
+        }
+        __syncwarp();                          // every lane has read the slot
+        if (e + TMA_NS < end) issue(e + TMA_NS);
     }
+    if (STATS && lane == 0) st[S_ITEM_EDGES] += end - beg;
 }
 
 template <bool STATS, bool BND = false>
@@ -851,13 +853,26 @@ __global__ void __launch_bounds__(256, TMA ? RPQ_TMA_MINB : RPQ_LEVEL_MINB) k_le
 }
 
 // Deferred long rows: a warp per HUB_EDGES-edge segment.
-template <bool STATS, bool BND = false>
-__global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A, const Layout *__restrict__ Sg,
-                                                                   const LevelArgs p) {
+template <bool STATS, bool BND = false, bool TMA = false>
+__global__ void __launch_bounds__(256, TMA ? RPQ_TMA_MINB : RPQ_HUB_MINB) k_level_hub(const DevAuto A,
+                                                                                    const Layout *__restrict__ Sg,
+                                                                                    const LevelArgs p) {
     if (BND && *(volatile const uint32_t *)&p.ctrl->blevel > p.level_lim) return;   // length bound reached
     __shared__ Layout S;
+    extern __shared__ __align__(128) unsigned char tma_dyn[];
     load_layout(S, Sg, A.nq);
     const int lane = threadIdx.x & 31;
+    TmaRing ring{};
+    if constexpr (TMA) {
+        unsigned char *wb = tma_dyn + (threadIdx.x >> 5) * TMA_WARP_BYTES;
+        ring.bar = reinterpret_cast<uint64_t *>(wb);
+        ring.buf = reinterpret_cast<uint64_t *>(wb + 64);
+        if (lane == 0) {
+            for (int sl = 0; sl < TMA_NS; ++sl) mbar_init(ring.bar + sl, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
     const uint32_t n = min(p.ctrl->nhub_recs, p.hrec_cap);
@@ -877,6 +892,16 @@ __global__ void __launch_bounds__(256, RPQ_HUB_MINB) k_level_hub(const DevAuto A
         uint64_t f[KGRP];
 #pragma unroll
         for (int k = 0; k < KGRP; ++k) f[k] = p.hubF[((uint64_t)r.hitem * KGRP + k) * 32 + lane];
+        if constexpr (TMA) {
+            const int nk = (int)h.nk;
+            const uint32_t c0 = (uint32_t)h.bits & 0xffu;
+            const uint32_t span = ((uint32_t)(h.bits >> (8 * (nk - 1))) & 0xffu) - c0 + 1u;
+            if (span <= (uint32_t)KGRP && (h.xw * 32u + c0 + span) * 32u <= p.nw) {
+                expand_edges_tma<STATS>(p, S, A.tto[r.t], A.nbr[A.tslot[r.t]], r.beg, r.end, f, h.bits, nk, c0, span,
+                                        h.xw, lane, st, act, A.toff[A.tto[r.t] + 1] > A.toff[A.tto[r.t]], ring);
+                continue;
+            }
+        }
         dispatch_edges<STATS, BND>((int)h.nk, p, S, A.tto[r.t], A.nbr[A.tslot[r.t]], r.beg, r.end, f, h.bits, h.xw, lane,
                               st, act, A.toff[A.tto[r.t] + 1] > A.toff[A.tto[r.t]]);
     }
@@ -2139,17 +2164,20 @@ cudaError_t build_level_graph(LevelGraph &LG, const DevAuto &A, const Layout *Sg
     const bool pull = P0.pull_mode != 0;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u0)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r0)) != cudaSuccess) return e;
-    void *lvl = P0.tma ? (void *)k_level<STATS, false, true> : (void *)k_level<STATS, BND>;
-    const int lgr = P0.tma ? 148 * RPQ_TMA_MINB : grid;
-    const unsigned lsm = P0.tma ? TMA_SMEM : 0u;
+    void *lvl = (P0.tma & 1u) ? (void *)k_level<STATS, false, true> : (void *)k_level<STATS, BND>;
+    const int lgr = (P0.tma & 1u) ? 148 * RPQ_TMA_MINB : grid;
+    const unsigned lsm = (P0.tma & 1u) ? TMA_SMEM : 0u;
     if ((e = add(lvl, dim3(lgr), dim3(256), a0, lsm)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a0)) != cudaSuccess) return e;
-    if (hub && (e = add((void *)k_level_hub<STATS, BND>, dim3(hgrid), dim3(256), a0)) != cudaSuccess) return e;
+    void *hubk = (P0.tma & 2u) ? (void *)k_level_hub<STATS, false, true> : (void *)k_level_hub<STATS, BND>;
+    const int hgr = (P0.tma & 2u) ? 148 * RPQ_TMA_MINB : hgrid;
+    const unsigned hsm = (P0.tma & 2u) ? TMA_SMEM : 0u;
+    if (hub && (e = add(hubk, dim3(hgr), dim3(256), a0, hsm)) != cudaSuccess) return e;
     if ((e = add((void *)k_units, dim3(ugrid), dim3(256), u1)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull_prep, dim3(148 * 8), dim3(256), r1)) != cudaSuccess) return e;
     if ((e = add(lvl, dim3(lgr), dim3(256), a1, lsm)) != cudaSuccess) return e;
     if (pull && (e = add((void *)k_pull<STATS>, dim3(148 * 8), dim3(256), a1)) != cudaSuccess) return e;
-    if (hub && (e = add((void *)k_level_hub<STATS, BND>, dim3(hgrid), dim3(256), a1)) != cudaSuccess) return e;
+    if (hub && (e = add(hubk, dim3(hgr), dim3(256), a1, hsm)) != cudaSuccess) return e;
     if ((e = add((void *)k_level_end, dim3(1), dim3(1), m1)) != cudaSuccess) return e;
     if (update) return ni == LG.nodes.size() ? cudaSuccess : cudaErrorInvalidValue;
     return cudaGraphInstantiate(&LG.exec, LG.g, 0);
@@ -2168,17 +2196,19 @@ rpq_status run_levels_host(const DevAuto &A, const Layout *Sg, const LevelArgs &
         if (P.pull_mode) k_pull_prep<<<148 * 8, 256, 0, s>>>(A, P);
         if (stats) {
             if (P.bounded) k_level<true, true><<<grid, 256, 0, s>>>(A, Sg, P);
-            else if (P.tma) k_level<true, false, true><<<148 * RPQ_TMA_MINB, 256, TMA_SMEM, s>>>(A, Sg, P);
+            else if (P.tma & 1u) k_level<true, false, true><<<148 * RPQ_TMA_MINB, 256, TMA_SMEM, s>>>(A, Sg, P);
             else k_level<true><<<grid, 256, 0, s>>>(A, Sg, P);
             if (P.pull_mode) k_pull<true><<<148 * 8, 256, 0, s>>>(A, Sg, P);
             if (hub && P.bounded) k_level_hub<true, true><<<hgrid, 256, 0, s>>>(A, Sg, P);
+            else if (hub && (P.tma & 2u)) k_level_hub<true, false, true><<<148 * RPQ_TMA_MINB, 256, TMA_SMEM, s>>>(A, Sg, P);
             else if (hub) k_level_hub<true><<<hgrid, 256, 0, s>>>(A, Sg, P);
         } else {
             if (P.bounded) k_level<false, true><<<grid, 256, 0, s>>>(A, Sg, P);
-            else if (P.tma) k_level<false, false, true><<<148 * RPQ_TMA_MINB, 256, TMA_SMEM, s>>>(A, Sg, P);
+            else if (P.tma & 1u) k_level<false, false, true><<<148 * RPQ_TMA_MINB, 256, TMA_SMEM, s>>>(A, Sg, P);
             else k_level<false><<<grid, 256, 0, s>>>(A, Sg, P);
             if (P.pull_mode) k_pull<false><<<148 * 8, 256, 0, s>>>(A, Sg, P);
             if (hub && P.bounded) k_level_hub<false, true><<<hgrid, 256, 0, s>>>(A, Sg, P);
+            else if (hub && (P.tma & 2u)) k_level_hub<false, false, true><<<148 * RPQ_TMA_MINB, 256, TMA_SMEM, s>>>(A, Sg, P);
             else if (hub) k_level_hub<false><<<hgrid, 256, 0, s>>>(A, Sg, P);
         }
         RPQ_CUDA_TRY(cudaMemcpyAsync(h_flag, &P.ctrl->active[par ^ 1], 4, cudaMemcpyDeviceToHost, s));
@@ -2916,15 +2946,18 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
     }
     P0.bounded = bounded ? 1u : 0u;
     {   // bulk-copy (TMA) expand: RPQ_TMA=1 (needs 32-word chunks; not with bounded or pull levels)
+        // RPQ_TMA = bit 0: k_level, bit 1: k_level_hub (e.g. 1, 2, 3)
         const char *et = getenv("RPQ_TMA");
-        P0.tma = (et && et[0] == '1' && !bounded && !P0.pull_mode && CW == 32) ? 1u : 0u;
+        const uint32_t tm = et ? (uint32_t)(atoi(et) & 3) : 0u;
+        P0.tma = (!bounded && !P0.pull_mode && CW == 32) ? tm : 0u;
         if (P0.tma) {
             static bool attr_set = false;
             if (!attr_set) {
-                cudaFuncSetAttribute((const void *)k_level<false, false, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
-                cudaFuncSetAttribute((const void *)k_level<true, false, true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
+                const void *fns[4] = {(const void *)k_level<false, false, true>, (const void *)k_level<true, false, true>,
+                                      (const void *)k_level_hub<false, false, true>,
+                                      (const void *)k_level_hub<true, false, true>};
+                for (const void *fn : fns)
+                    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TMA_SMEM);
                 attr_set = true;
             }
         }

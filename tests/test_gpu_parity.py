@@ -341,18 +341,27 @@ def test_sparse_batches_dense_engine(monkeypatch):
         assert_pairs_equal(r.rows(), want, rx)
 
 
+@pytest.mark.parametrize("tma", ["1", "2", "3"])
 @pytest.mark.parametrize("B", [0, 4096])
-def test_tma_bulk_copy_expand(B, monkeypatch):
-    """RPQ_TMA=1: the target-row segments of KC >= 2 chunk groups arrive by
-    cp.async.bulk into a per-warp shared-memory ring (mbarrier completion);
-    pairs and PE must equal the oracle's (multi-chunk rows: B = 0 puts all
-    20 K sources in one batch, 10 chunks per row)."""
-    monkeypatch.setenv("RPQ_TMA", "1")
+def test_tma_bulk_copy_expand(B, tma, monkeypatch):
+    """RPQ_TMA (bit 0: k_level, bit 1: k_level_hub): the target-row segments
+    of multi-chunk groups arrive by cp.async.bulk into a per-warp shared-memory
+    ring (mbarrier completion); pairs and PE must equal the oracle's
+    (multi-chunk rows: B = 0 puts all 20 K sources in one batch, 10 chunks
+    per row; vertices 0 and 7 have 1,500 / 900 out-edges, so their rows are
+    split into HUB_EDGES segments for the hub kernel)."""
+    monkeypatch.setenv("RPQ_TMA", tma)
     monkeypatch.setenv("RPQ_ENGINE", "dense")
+    rng = np.random.default_rng(12)
     g = synth.random_graph(20000, 70000, 3, seed=12)
+    hs = np.concatenate([np.zeros(1500, np.uint32), np.full(900, 7, np.uint32)])
+    hd = rng.integers(0, 20000, hs.size).astype(np.uint32)
+    hl = np.concatenate([np.zeros(1500, np.uint16), np.ones(900, np.uint16)])
+    g = synth.Graph(20000, np.concatenate([g.src, hs]), np.concatenate([g.dst, hd]), np.concatenate([g.label, hl]),
+                    g.label_names).check()
     G = R.rpq_graph_load(g)
     for rx in ["a*", "(a|b)*c", "a b* c"]:
         want, o = oracle_rows(g, rx)
         r = gpu_eval(G, rx, R.RPQ_PAIRS | R.RPQ_STATS, batch_sources=B)
-        assert_pairs_equal(r.rows(), want, (rx, B))
-        assert r.stats()["product_edges"] == int(o["pe"].sum()), rx
+        assert_pairs_equal(r.rows(), want, (rx, B, tma))
+        assert r.stats()["product_edges"] == int(o["pe"].sum()), (rx, tma)
