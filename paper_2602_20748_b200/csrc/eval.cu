@@ -2831,6 +2831,7 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
                     int herr = 0;
                     RPQ_CUDA_TRY(cudaMemcpyAsync(&herr, d_err, sizeof(int), cudaMemcpyDeviceToHost, s));
                     RPQ_CUDA_TRY(cudaStreamSynchronize(s));
+                    if (getenv("RPQ_TEST_SPARSE_REDO")) herr = 1;   // test hook: exercise the fallback below
                     rpq_result_release(sub_keep);
                     sub_keep = nullptr;
                     if (herr) {   // rare: redo the whole query on the dense engine

@@ -365,3 +365,19 @@ def test_tma_bulk_copy_expand(B, tma, monkeypatch):
         r = gpu_eval(G, rx, R.RPQ_PAIRS | R.RPQ_STATS, batch_sources=B)
         assert_pairs_equal(r.rows(), want, (rx, B, tma))
         assert r.stats()["product_edges"] == int(o["pe"].sum()), (rx, tma)
+
+
+def test_sparse_write_pass_redo(monkeypatch):
+    """If the sparse engine's PAIRS write pass overflows where its counting
+    pass fitted, the whole query is re-run on the dense engine.  The hook
+    RPQ_TEST_SPARSE_REDO forces that path: pairs and PE must still equal the
+    oracle's (sparse-reach and dense-reach queries)."""
+    monkeypatch.setenv("RPQ_ENGINE", "sparse")
+    monkeypatch.setenv("RPQ_TEST_SPARSE_REDO", "1")
+    g = synth.random_graph(3000, 6000, 3, seed=31)
+    G = R.rpq_graph_load(g)
+    for rx in ["a b c", "c?a", "(a|b)*c*"]:
+        want, o = oracle_rows(g, rx)
+        r = gpu_eval(G, rx, R.RPQ_PAIRS | R.RPQ_STATS)
+        assert_pairs_equal(r.rows(), want, rx)
+        assert r.stats()["product_edges"] == int(o["pe"].sum()), rx
