@@ -66,6 +66,12 @@ constexpr int NSTAT = 14;
 #ifndef RPQ_HUB_MINB
 #define RPQ_HUB_MINB 4
 #endif
+#ifndef RPQ_LS_MAX
+#define RPQ_LS_MAX 5          // a work unit splits into at most 2^RPQ_LS_MAX tickets ...
+#endif
+#ifndef RPQ_LS_WARPS
+#define RPQ_LS_WARPS 8        // ... until there are RPQ_LS_WARPS tickets per warp of the grid
+#endif
 #ifndef RPQ_SLOTS
 #define RPQ_SLOTS 8
 #endif
@@ -696,7 +702,7 @@ __global__ void __launch_bounds__(256, TMA ? RPQ_TMA_MINB : RPQ_LEVEL_MINB) k_le
     // 32 >> ls X words so that every warp of the grid gets work; a ticket is
     // one atomic on the level's cursor.
     int ls = 0;
-    while (ls < 5 && ((uint64_t)nunits << ls) < nwarps * 8) ++ls;
+    while (ls < RPQ_LS_MAX && ((uint64_t)nunits << ls) < nwarps * RPQ_LS_WARPS) ++ls;
     const uint32_t ntk = nunits << ls;
     const int part_lanes = 32 >> ls;
     for (;;) {

@@ -30,7 +30,7 @@ G = R.rpq_graph_load(g, stream=s.cuda_stream, in_edges=os.environ.get("TV_IN_EDG
 tag = os.path.basename(os.environ.get("RPQ_LIB_PATH", "librpq.so"))
 for rx in qs:
     a = R.rpq_compile(G, rx)
-    B = R.rpq_plan(G, a, stream=s.cuda_stream)["batch_sources"] if shards > 1 else 0
+    B = R.rpq_plan(G, a, stream=s.cuda_stream, shard_count=shards)["batch_sources"] if shards > 1 else 0
     R.rpq_eval_allpairs(G, a, mode=R.RPQ_COUNT, stream=s.cuda_stream, shard_count=shards, batch_sources=B)
     best = None
     for _ in range(3 if not wl.startswith("rmat") else 1):
