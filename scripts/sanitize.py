@@ -52,4 +52,10 @@ os.environ["RPQ_PULL"] = "always"
 check(G, g, "(a|b)*c", batch_sources=2048)
 os.environ.pop("RPQ_PULL")
 check(G, g, "a b* c", batch_sources=256, max_hops=3)
+# TMA bulk-copy ring in k_level and k_level_hub (all 5,000 sources: 3 chunks per row)
+os.environ["RPQ_ENGINE"] = "dense"
+os.environ["RPQ_TMA"] = "3"
+check(G, g, "(a|b)*c*")
+os.environ.pop("RPQ_TMA")
+os.environ.pop("RPQ_ENGINE")
 print("sanitize workload OK")
