@@ -473,6 +473,12 @@ def north_star_leg(args, R, D, maker, sp, stream, local, rank, world, allmax, al
     peak, peak_src = load_peaks()
     traffic = load_traffic("cfg5")
     alg_bytes = bytes_per_pe * pe
+    ncu_over_alg = None
+    if traffic and traffic.get("all") and pst.get("levels"):
+        kl = traffic["all"]
+        dram_per_level = sum(kl[k]["dram_bytes"] for k in ("k_level", "k_level_hub") if k in kl) / \
+            max(1, kl["k_level"]["launches"])
+        ncu_over_alg = dram_per_level / (algorithmic_bytes(pst) / pst["levels"])
     # per GPU: its share of the bytes over the whole-query time (the slowest rank)
     achieved = alg_bytes / world / (ms / 1e3) / 1e9
     out = {"workload": "cfg5", "graph": WORKLOADS["cfg5"]["desc"], "query": rx, "mode": "COUNT, all-pairs, all batches",
@@ -484,9 +490,10 @@ def north_star_leg(args, R, D, maker, sp, stream, local, rank, world, allmax, al
                         "achieved_per_gpu": achieved, "frac": achieved / peak,
                         "note": "algorithmic bytes per PE from an RPQ_STATS probe of 1/64 of the batches x exact PE; "
                                 "time = whole query (count pass, clears, per-batch setup included), slowest rank",
-                        "ncu_dram_over_algorithmic": (traffic["dram_bytes_per_launch"] /
-                                                      traffic["algorithmic_bytes_per_launch"])
-                        if traffic and traffic.get("algorithmic_bytes_per_launch") else None},
+                        # ncu DRAM bytes of the level kernels (k_level + k_level_hub) per level on
+                        # shard 0 of 64 (profiles/traffic_cfg5.json) over this run's algorithmic
+                        # bytes per level on the same shard (the RPQ_STATS probe above, rank 0)
+                        "ncu_dram_over_algorithmic": ncu_over_alg},
            "clocks": clk.summary()}
     if not out["count_ok"] and rank == 0:
         print(f"north_star: count {d.count} != expected {RMAT24_COUNT}", file=sys.stderr)
