@@ -358,7 +358,9 @@ def run_ours(args):
     step_bytes = probe_bytes * args.steps
     achieved = step_bytes / (agg["expand_ms"] / 1e3) / 1e9 if agg["expand_ms"] > 0 else None
     per_launch = probe_bytes / max(1, probe_levels)
-    traffic = load_traffic(args.workload)
+    # the committed ncu bytes per launch are for full-width batches; a sampled
+    # shard (--sample-shards) runs narrower batches, so they do not apply
+    traffic = load_traffic(args.workload) if sample == 1 else None
     line = {
         "metric": "all-pairs RPQ product-edges traversed/s",
         "value": value,

@@ -57,13 +57,16 @@ def main():
         if fn.startswith("traffic_") and fn.endswith(".csv"):
             wl = fn[len("traffic_"):-4]
             T = summarise("traffic", os.path.join(d, fn))
-            k = T["k_level"]
+            # the workload's dominant level kernel (k_level; k_pull for cfg3's bottom-up knows+)
+            kname = max((n for n in T if n in ("k_level", "k_pull")), key=lambda n: T[n]["time_us"])
+            k = T[kname]
             shards = " 64" if wl == "cfg5" else ""
             with open(os.path.join(pdir, f"traffic_{wl}.json"), "w") as f:
-                json.dump({"kernel": "k_level", "dram_bytes_per_launch": k["dram_bytes_per_launch"],
+                json.dump({"kernel": kname, "dram_bytes_per_launch": k["dram_bytes_per_launch"],
                            "launches": k["launches"], "round": tag,
                            "source": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum "
-                                     f"-k regex:k_level over one COUNT evaluation of each {wl} query "
+                                     f"-k regex:'k_level|k_pull|k_count_total|k_clear_dense' over one COUNT "
+                                     f"evaluation of each {wl} query "
                                      f"(scripts/prof_workload.py {wl}{shards}, RPQ_HOST_LOOP=1, PROF_NOSTATS=1)",
                            "all": T}, f, indent=1)
         if fn.startswith("full_") and fn.endswith(".ncu-rep"):
