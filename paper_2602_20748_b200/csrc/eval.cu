@@ -104,6 +104,14 @@ struct Layout {
     uint32_t len[MAXQ];
 };
 
+#ifndef RPQ_HUB_LOADS
+#define RPQ_HUB_LOADS 512      // visited-word loads per lane in one hub record (edges x active chunks)
+#endif
+__host__ __device__ __forceinline__ uint32_t hub_seglen(int nk) {
+    const uint32_t l = (uint32_t)RPQ_HUB_LOADS / (uint32_t)(nk > 0 ? nk : 1);
+    return l < 32u ? 32u : (l > 512u ? 512u : l);      // <= HUB_EDGES
+}
+
 struct HubItem {                // a deferred row-group (frontier words in hubF)
     uint32_t row;              // global row (state, vertex)
     uint32_t xw;               // X word of the row (chunk block of 32)
@@ -821,14 +829,17 @@ __global__ void __launch_bounds__(256, TMA ? RPQ_TMA_MINB : RPQ_LEVEL_MINB) k_le
                             }
                         }
                         if (hslot >= 0) {
-                            const uint32_t nseg = (end - beg + HUB_EDGES - 1) / HUB_EDGES;
+                            // records of ~HUB_LOADS visited-word loads per lane: fewer
+                            // edges per record when more chunks are active
+                            const uint32_t seglen = hub_seglen(nk);
+                            const uint32_t nseg = (end - beg + seglen - 1) / seglen;
                             uint32_t r = 0;
                             if (lane == 0) r = atomicAdd(&p.ctrl->nhub_recs, nseg);
                             r = __shfl_sync(0xffffffffu, r, 0);
                             if (r + nseg <= p.hrec_cap) {
                                 for (uint32_t sg = lane; sg < nseg; sg += 32) {
-                                    const uint32_t b0 = beg + sg * HUB_EDGES;
-                                    p.hrecs[r + sg] = HubRec{(uint32_t)hslot, (uint32_t)t, b0, min(end, b0 + HUB_EDGES)};
+                                    const uint32_t b0 = beg + sg * seglen;
+                                    p.hrecs[r + sg] = HubRec{(uint32_t)hslot, (uint32_t)t, b0, min(end, b0 + seglen)};
                                 }
                                 continue;
                             }
