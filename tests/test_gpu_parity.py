@@ -381,3 +381,30 @@ def test_sparse_write_pass_redo(monkeypatch):
         r = gpu_eval(G, rx, R.RPQ_PAIRS | R.RPQ_STATS)
         assert_pairs_equal(r.rows(), want, rx)
         assert r.stats()["product_edges"] == int(o["pe"].sum()), rx
+
+
+def test_edgeless_graph_and_empty_vertex_set():
+    """|E| = 0: every query returns exactly its epsilon pairs (R1), and
+    nothing else; |V| = 0 is rejected with EINVAL."""
+    g = synth.Graph(1000, np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.uint16), ["a", "b"]).check()
+    G = R.rpq_graph_load(g)
+    for rx, n in [("a*", 1000), ("a+", 0), ("(a|b)*b?", 1000), ("ab", 0)]:
+        assert gpu_eval(G, rx, R.RPQ_COUNT).count == n, rx
+        r = gpu_eval(G, rx, R.RPQ_PAIRS)
+        assert r.count == n and (n == 0 or np.array_equal(r.rows(), np.stack([np.arange(n)] * 2, 1))), rx
+    with pytest.raises(R.RPQError):
+        R.rpq_graph_load(synth.Graph(0, np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.uint16),
+                                     ["a"]))
+
+
+def test_many_state_automata_multi_chunk():
+    """Automata with 6-9 minimal-DFA states over 10 chunks per row (all 20 K
+    sources in one batch): pairs and PE equal O1's."""
+    g = synth.random_graph(20000, 60000, 4, seed=41)
+    G = R.rpq_graph_load(g)
+    for rx in ["a b c d a", "(a|b)(b|c)(c|d)d*a", "a(b a)*c(d|a)+", "((a b)|(c d))+ a?"]:
+        a = R.rpq_compile(G, rx)
+        want, o = oracle_rows(g, rx)
+        r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_PAIRS | R.RPQ_STATS)
+        assert_pairs_equal(r.rows(), want, rx)
+        assert r.stats()["product_edges"] == int(o["pe"].sum()), rx
