@@ -1859,131 +1859,186 @@ __global__ void k_fill_eps(unsigned long long *cand_cnt, uint64_t n, unsigned lo
         cand_cnt[j] = val;
 }
 
-// Write sorted (src, dst) pairs.  A warp takes one (TILE_V-vertex tile,
-// word) task = 64 sources: (1) warp bit transposes give, per source, the masks
-// of the tile's 32-vertex blocks (shared memory); (2) per source, the warp
-// expands its tile mask into the run of its targets in shared memory and
-// writes the run with 16-byte vector stores (one (src, dst) pair = 2 x 4 B).
-// Each source's tile run is contiguous (start + per-tile scan), so every
-// output sector is written whole by one warp at one time (per-bit scattered
-// writes across 256 sources kept ~10^6 partial runs open and doubled the DRAM
-// traffic through L2 evictions; a store per 32-vertex block and source cost
-// ~34 instructions per block: 10.8 G per cfg2 launch).  The per-source run
-// starts (pidx -> start, per-tile scan, source id) are fetched for all 64
-// sources at once before phase 2 (they were 64 dependent load chains), and
-// TILE_V = 512 keeps the masks at 4 KB per warp (occupancy was limited by
-// shared memory at 24 warps per SM with 1024-vertex tiles).
 constexpr int WP_WARPS = 4;
 constexpr int WP_BLK = TILE_V / 32;          // 32-vertex blocks per tile
 constexpr int WP_LD = WP_BLK + 1;            // padded row of masks (no bank conflicts)
-__global__ void __launch_bounds__(WP_WARPS * 32)
+// Write sorted (src, dst) pairs.  A CTA (4 warps) takes a group of 4
+// consecutive words (256 sources) and a PART of tpp consecutive tiles, and
+// walks the part tile by tile with each source's output offset kept in a
+// register, so a source's whole part is ONE contiguous run written by one
+// warp in order (no partial sectors between tiles).  Per tile:
+//   (1) the CTA loads the 512 x 4 visited words (OR over the final states)
+//       with each 32-byte row sector fetched by 4 adjacent lanes of one
+//       request (a warp reading one word of 32 rows used 8 of 32 bytes
+//       per sector) into shared memory;
+//   (2) warp w transposes ITS word's row (bit transposes give, per source,
+//       the masks of the tile's 32-vertex blocks) and keeps the masks in
+//       place of that row (padded rows, conflict-free);
+//   (3) per source, block by block, the lanes with a set bit write their
+//       vertex to base + rank (rank = popcount of the lower lanes' bits) of
+//       a per-warp staging buffer (consecutive words: no bank conflicts),
+//       and ONE TMA bulk store (cp.async.bulk shared -> global) writes the
+//       16-B-aligned body of the run; two buffers per warp, so the next
+//       source is staged while the store drains.  Per-block global stores
+//       instead serialised on the store address registers.  The source
+//       column is a run of one value (16-byte vector stores).
+// Offsets: start of the candidate + exclusive per-tile scan at the part's
+// first tile, then + the source's count of every tile.
+constexpr int WP3_XLD = TILE_V + 40;         // xs row: words k, k+1 in disjoint bank halves; holds 64 x WP_LD masks
+__device__ __forceinline__ int wp_swz(int b, int blk) { return b * WP_LD + blk; }   // padded rows: conflict-free, immediate offsets
+static_assert(WP3_XLD * 8 >= 64 * WP_LD * 4 && (WP3_XLD * 2) % 32 == 16, "xs row layout");
+// TMA bulk store (smem -> global, 16-B aligned, size a multiple of 16) and its
+// completion group (waiting for .read only frees the shared-memory source)
+__device__ __forceinline__ void bulk_s2g(void *gdst, const void *ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(smem_u32(ssrc)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+constexpr int WP_STG = TILE_V + 8;            // staging buffer of one source's tile run (u32, 16-B multiple)
+
+__global__ void __launch_bounds__(WP_WARPS * 32, 6)
 k_write_pairs(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn, uint32_t nw,
-              uint32_t nb, uint32_t nseg, const uint32_t *cnt_scan, const uint32_t *cand, const uint32_t *pidx,
-              uint64_t b0, const unsigned long long *start, uint64_t jlo, uint32_t *osrc, uint32_t *odst) {
-    __shared__ uint32_t masks_s[WP_WARPS][64 * WP_LD];
-    __shared__ __align__(16) uint32_t buf_s[WP_WARPS][TILE_V + 8];
+               uint32_t nb, uint32_t nseg, uint32_t tpp, const uint32_t *cnt_scan, const uint32_t *cand,
+               const uint32_t *pidx, uint64_t b0, const unsigned long long *start, uint64_t jlo, uint32_t *osrc,
+               uint32_t *odst) {
+    __shared__ __align__(16) uint64_t xs[4][WP3_XLD];
+    __shared__ __align__(16) uint32_t stage_s[WP_WARPS][2][WP_STG];
+    __shared__ uint32_t carry_s[WP_WARPS][64][8];                  // < 8 carried targets per source
     const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-    uint32_t *masks = masks_s[wl];
-    // a CTA takes WP_WARPS consecutive words of one tile (warp wl: word
-    // w4 * WP_WARPS + wl), so the 32-byte sectors of a vertex row are read by
-    // its warps together (L1 hits) instead of by four drifting warps, each of
-    // which missed in an L2 flooded by the output writes (12 GB of reads per
-    // cfg2 launch for 1.15 GB of visited words)
-    const uint64_t nw4 = (nw + WP_WARPS - 1) / WP_WARPS;
-    for (uint64_t ct = blockIdx.x; ct < (uint64_t)nseg * nw4; ct += gridDim.x) {
-      const uint32_t seg = (uint32_t)(ct / nw4);
-      const uint32_t w = (uint32_t)(ct % nw4) * WP_WARPS + (uint32_t)wl;
-      if (w < nw) {
-        const uint64_t vbeg = (uint64_t)seg * TILE_V, vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
-        const int nblk = (int)((vend - vbeg + 31) / 32);
-        // run start and source id of sources 64w + lane and 64w + 32 + lane
+    int sbuf = 0;                                                  // staging buffer of the next source
+    const int t = (int)threadIdx.x;
+    const uint32_t lt = (1u << lane) - 1u;
+    const bool vec_ok = ((reinterpret_cast<uintptr_t>(osrc) | reinterpret_cast<uintptr_t>(odst)) & 15u) == 0;
+    const uint64_t nwg = (nw + 3) / 4;
+    const uint64_t nparts = (nseg + tpp - 1) / tpp;
+    const uint32_t k = (uint32_t)t & 3u, r = (uint32_t)t >> 2;    // this thread's word / first vertex of a tile
+    for (uint64_t ct = blockIdx.x; ct < nwg * nparts; ct += gridDim.x) {
+        // word-group-minor: concurrently running CTAs read neighbouring
+        // sectors of the same rows
+        const uint32_t g = (uint32_t)(ct % nwg);
+        const uint32_t s0 = (uint32_t)(ct / nwg) * tpp, s1 = min(nseg, s0 + tpp);
+        const uint32_t w = g * 4 + (uint32_t)wl, wk = g * 4 + k;
         unsigned long long o_lo = 0, o_hi = 0;
-        uint32_t sid_lo = 0, sid_hi = 0;
+        uint32_t sid_lo = 0, sid_hi = 0, cc_lo = 0, cc_hi = 0;
         {
             const uint32_t i0 = w * 64 + (uint32_t)lane, i1 = i0 + 32;
-            if (i0 < nb) {
+            if (w < nw && i0 < nb) {
                 const uint32_t j = pidx[b0 + i0];
-                o_lo = start[j - jlo] + cnt_scan[(uint64_t)i0 * nseg + seg];
+                o_lo = start[j - jlo] + cnt_scan[(uint64_t)i0 * nseg + s0];
                 sid_lo = cand[j];
             }
-            if (i1 < nb) {
+            if (w < nw && i1 < nb) {
                 const uint32_t j = pidx[b0 + i1];
-                o_hi = start[j - jlo] + cnt_scan[(uint64_t)i1 * nseg + seg];
+                o_hi = start[j - jlo] + cnt_scan[(uint64_t)i1 * nseg + s0];
                 sid_hi = cand[j];
             }
         }
-        // (1) masks[b][blk]: which of the 32 vertices of block blk source b reaches
-        for (int bk = 0; bk < WP_BLK; bk += 8) {
-            uint64_t xs[8];
+        for (uint32_t seg = s0; seg < s1; ++seg) {
+            const uint64_t vbeg = (uint64_t)seg * TILE_V;
+            {
+                const uint64_t vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
+                uint64_t xv[WP_BLK];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int blk = bk + k;
-                const uint64_t vv = vbeg + (uint64_t)blk * 32 + lane;
-                xs[k] = (blk < nblk && vv < vend) ? ans_word<true>(A, S, Vis, vlo + (uint32_t)vv, w, nw) : 0ull;
+                for (int i = 0; i < WP_BLK; ++i) xv[i] = 0ull;
+                uint64_t fm = wk < nw ? A.final_mask : 0ull;
+                while (fm) {
+                    const int q = __ffsll((long long)fm) - 1;
+                    fm &= fm - 1;
+                    const uint32_t qlo = S.lo[q], qlen = S.len[q];
+                    const uint64_t qb = S.row_base[q];
+#pragma unroll
+                    for (int i = 0; i < WP_BLK; ++i) {
+                        const uint64_t vv = vbeg + r + 32u * (uint32_t)i;
+                        const uint32_t d = vlo + (uint32_t)vv - qlo;
+                        if (vv < vend && d < qlen) xv[i] |= ld_cg(Vis + (qb + d) * nw + wk);
+                    }
+                }
+                __syncthreads();                 // every warp is done with the previous tile's masks
+#pragma unroll
+                for (int i = 0; i < WP_BLK; ++i) xs[k][r + 32u * (uint32_t)i] = xv[i];
+                __syncthreads();
             }
+            // (2) this warp's word row -> per-source block masks, in place
+            uint64_t xr[WP_BLK];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                // lane b keeps the masks of sources b and b + 32
-                masks[lane * WP_LD + bk + k] = warp_transpose32((uint32_t)xs[k], lane);
-                masks[(lane + 32) * WP_LD + bk + k] = warp_transpose32((uint32_t)(xs[k] >> 32), lane);
-            }
-        }
-        __syncwarp();
-        // (2) per source b: its TILE_V-bit tile mask -> the run of its targets
-        // staged in shared memory (lane l expands bits [16 l, 16 l + 16) after
-        // a warp scan of the lanes' popcounts), then both columns written with
-        // 16-byte vector stores.  The run is staged at index (o mod 4) so that
-        // the 16-byte-aligned part of the global run maps to aligned shared
-        // vectors (conflict-free LDS.128).
-        uint32_t *buf = buf_s[wl];
-        const bool vec_ok = ((reinterpret_cast<uintptr_t>(osrc) | reinterpret_cast<uintptr_t>(odst)) & 15u) == 0;
-        const uint32_t vb = vlo + (uint32_t)vbeg + (uint32_t)lane * 16u;
-        for (int b = 0; b < 64; ++b) {
-            const uint32_t i = w * 64 + (uint32_t)b;
-            if (i >= nb) break;
-            const unsigned long long o = __shfl_sync(0xffffffffu, b < 32 ? o_lo : o_hi, b & 31);
-            const uint32_t sid = __shfl_sync(0xffffffffu, b < 32 ? sid_lo : sid_hi, b & 31);
-            const int blk = lane >> 1;
-            uint32_t x = blk < nblk ? masks[b * WP_LD + blk] : 0u;
-            x = (lane & 1) ? (x >> 16) : (x & 0xffffu);
-            const uint32_t c = (uint32_t)__popc(x);
-            uint32_t incl = c;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += y;
-            }
-            const uint32_t n = __shfl_sync(0xffffffffu, incl, 31);
-            if (n == 0) continue;
-            const uint32_t off = (uint32_t)(o & 3ull);
-            uint32_t pos = off + incl - c;
-#pragma unroll
-            for (int bt = 0; bt < 16; ++bt)
-                if ((x >> bt) & 1u) buf[pos++] = vb + (uint32_t)bt;
+            for (int blk = 0; blk < WP_BLK; ++blk) xr[blk] = xs[wl][blk * 32 + lane];
             __syncwarp();
-            if (!vec_ok) {                                        // unaligned caller buffers
-                for (uint32_t k = (uint32_t)lane; k < n; k += 32) { osrc[o + k] = sid; odst[o + k] = buf[off + k]; }
+            uint32_t *masks = reinterpret_cast<uint32_t *>(&xs[wl][0]);
+#pragma unroll
+            for (int blk = 0; blk < WP_BLK; ++blk) {
+                masks[wp_swz(lane, blk)] = warp_transpose32((uint32_t)xr[blk], lane);
+                masks[wp_swz(lane + 32, blk)] = warp_transpose32((uint32_t)(xr[blk] >> 32), lane);
+            }
+            __syncwarp();
+            if (w >= nw) continue;
+            // (3) per source of the warp's word.  Only whole 32-byte sectors
+            // are written before the part's last tile: the < 8 trailing
+            // targets of a tile run are carried (shared memory) to the next
+            // tile's run of the same source, so no sector is written in two
+            // halves far apart in time (L2 evicted such halves and HBM did a
+            // read-modify-write: ~4 GB of extra reads per cfg2 a* launch).
+            const bool last = seg + 1 == s1;
+            const uint32_t vb = vlo + (uint32_t)vbeg + (uint32_t)lane;
+            for (int b = 0; b < 64; ++b) {
+                const uint32_t i = w * 64 + (uint32_t)b;
+                if (i >= nb) break;
+                // o = global index of the source's first unwritten (carried) target
+                const unsigned long long o = __shfl_sync(0xffffffffu, b < 32 ? o_lo : o_hi, b & 31);
+                const uint32_t cc = __shfl_sync(0xffffffffu, b < 32 ? cc_lo : cc_hi, b & 31);
+                uint32_t *stg = stage_s[wl][sbuf];
+                uint32_t *cry = carry_s[wl][b];
+                const uint32_t off = (uint32_t)(o & 3ull);     // staged at (o mod 4): 16-B-aligned body
+                if (lane == 0) bulk_wait_read<1>();            // the bulk store that last read this buffer is done
                 __syncwarp();
-                continue;
+                if ((uint32_t)lane < cc) stg[off + lane] = cry[lane];
+                uint32_t n = cc;
+#pragma unroll
+                for (int blk = 0; blk < WP_BLK; ++blk) {
+                    const uint32_t m = masks[wp_swz(b, blk)];
+                    if ((m >> lane) & 1u) stg[off + n + (uint32_t)__popc(m & lt)] = vb + 32u * (uint32_t)blk;
+                    n += (uint32_t)__popc(m);
+                }
+                // write [0, end): everything on the last tile, else up to the
+                // last sector boundary of the run
+                const uint64_t ea = (o + n) & ~7ull;
+                const uint32_t end = last ? n : (ea > o ? (uint32_t)(ea - o) : 0u);
+                __syncwarp();
+                if ((uint32_t)lane < n - end) cry[lane] = stg[off + end + lane];
+                if (lane == (b & 31)) {                       // running position / carry of source b
+                    if (b < 32) { o_lo += end; cc_lo = n - end; }
+                    else { o_hi += end; cc_hi = n - end; }
+                }
+                if (end == 0) continue;
+                const uint32_t sid = __shfl_sync(0xffffffffu, b < 32 ? sid_lo : sid_hi, b & 31);
+                uint32_t *dp = odst + o, *sp = osrc + o;
+                if (!vec_ok) {
+                    for (uint32_t e = (uint32_t)lane; e < end; e += 32) { dp[e] = stg[off + e]; sp[e] = sid; }
+                    continue;
+                }
+                const uint32_t h = min(end, (4u - off) & 3u);              // head up to 16-B alignment
+                const uint32_t nv = (end - h) >> 2;                         // 16-B vectors
+                const uint32_t t0 = h + 4u * nv;                            // tail (< 4 elements)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    if (nv) bulk_s2g(dp + h, stg + off + h, nv * 16u);
+                    bulk_commit();
+                }
+                sbuf ^= 1;
+                if ((uint32_t)lane < h) { dp[lane] = stg[off + lane]; sp[lane] = sid; }
+                if (t0 + (uint32_t)lane < end) { dp[t0 + lane] = stg[off + t0 + lane]; sp[t0 + lane] = sid; }
+                uint4 *vs = reinterpret_cast<uint4 *>(sp + h);
+                const uint4 sv = make_uint4(sid, sid, sid, sid);
+                for (uint32_t e = (uint32_t)lane; e < nv; e += 32) vs[e] = sv;
             }
-            const uint32_t h = min(n, (4u - off) & 3u);          // head up to 16-B alignment
-            if ((uint32_t)lane < h) { osrc[o + lane] = sid; odst[o + lane] = buf[off + lane]; }
-            const uint32_t nvec = (n - h) >> 2;
-            uint4 *vs = reinterpret_cast<uint4 *>(osrc + o + h);
-            uint4 *vd = reinterpret_cast<uint4 *>(odst + o + h);
-            const uint4 *bv = reinterpret_cast<const uint4 *>(buf + (off ? 4u : 0u));
-            const uint4 sv = make_uint4(sid, sid, sid, sid);
-            for (uint32_t k = (uint32_t)lane; k < nvec; k += 32) {
-                vd[k] = bv[k];
-                vs[k] = sv;
-            }
-            const uint32_t t0 = h + 4u * nvec;                    // tail (< 4 elements)
-            if (t0 + (uint32_t)lane < n) { osrc[o + t0 + lane] = sid; odst[o + t0 + lane] = buf[off + t0 + lane]; }
-            __syncwarp();
         }
-      }
-      __syncthreads();
+        __syncthreads();                         // every warp is done with the masks
     }
+    if (lane == 0) bulk_wait_all();              // bulk stores complete before the CTA exits
 }
 
 // epsilon pairs (v, v) of non-productive candidates in [jlo, jhi)
@@ -3282,8 +3337,14 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             blocks.push_back(bl);
             HM("pairs: cudaMalloc of the block");
             if (vn) {
-                k_write_pairs<<<grid_for((uint64_t)nseg * nw * 32, WP_WARPS * 32, 148 * 16), WP_WARPS * 32, 0, s>>>(
-                    A, S, Vis, vlo, vn, (uint32_t)nw, nb, nseg, cnt, cand, pidx, b0, start, jlo, bl.src, bl.dst);
+                // parts of tpp tiles: ~24 CTA tasks per SM slot for balance
+                const uint64_t nwg = (nw + 3) / 4;
+                const uint64_t want = (uint64_t)148 * 6 * 4;
+                const uint64_t nparts = std::min<uint64_t>(nseg, (want + nwg - 1) / nwg);
+                const uint32_t tpp = (uint32_t)((nseg + nparts - 1) / nparts);
+                const uint64_t ntask = nwg * ((nseg + tpp - 1) / tpp);
+                k_write_pairs<<<(unsigned)std::min<uint64_t>(ntask, 148 * 6), WP_WARPS * 32, 0, s>>>(
+                    A, S, Vis, vlo, vn, (uint32_t)nw, nb, nseg, tpp, cnt, cand, pidx, b0, start, jlo, bl.src, bl.dst);
                 ST.kernel_launches++;
             }
             if (eps) {
