@@ -515,6 +515,7 @@ static rpq_status crpq_impl(const rpq_graph *g, const crpq_query *q, const rpq_e
 
 extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const rpq_eval_opts *opts_in,
                                 rpq_result **out) {
+    NvtxRange nvtx_("crpq_eval");
     if (out) *out = nullptr;
     if (!g || !q || !out) return rpq_fail(RPQ_EINVAL, "crpq_eval: NULL argument");
     std::vector<uint32_t> all(q->num_vars);
@@ -524,6 +525,7 @@ extern "C" rpq_status crpq_eval(const rpq_graph *g, const crpq_query *q, const r
 
 extern "C" rpq_status crpq_eval_project(const rpq_graph *g, const crpq_query *q, const uint32_t *out_vars,
                                         uint32_t num_out, const rpq_eval_opts *opts_in, rpq_result **out) {
+    NvtxRange nvtx_("crpq_eval_project");
     if (out) *out = nullptr;
     if (!g || !q || !out || !out_vars || num_out == 0) return rpq_fail(RPQ_EINVAL, "crpq_eval_project: bad argument");
     std::vector<uint32_t> ov(out_vars, out_vars + num_out);
@@ -871,6 +873,7 @@ static rpq_status crpq_impl(const rpq_graph *g, const crpq_query *q, const rpq_e
 // worst-case-optimal join (its matching order starts at u, w: the middle).
 extern "C" rpq_status rpq_eval_middle(const rpq_graph *g, const char *alpha, const char *mid, const char *beta,
                                       const rpq_eval_opts *opts, rpq_result **out) {
+    NvtxRange nvtx_("rpq_eval_middle");
     if (out) *out = nullptr;
     if (!g || !alpha || !mid || !beta || !out) return rpq_fail(RPQ_EINVAL, "rpq_eval_middle: NULL argument");
     rpq_nfa *na = nullptr, *nm = nullptr, *nb = nullptr;

@@ -2066,6 +2066,7 @@ struct PhaseTimer {
         mark("begin");
     }
     void mark(const char *what) {
+        nvtxMarkA(what);                 // phase boundary on the NVTX timeline
         if (ev) {
             cudaEvent_t e;
             cudaEventCreate(&e);
@@ -3499,6 +3500,7 @@ static rpq_status check_common(const rpq_graph *g, const rpq_nfa *a, rpq_result 
 
 extern "C" rpq_status rpq_eval_allpairs(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
                                         rpq_result **out) {
+    NvtxRange nvtx_("rpq_eval_allpairs");
     rpq_status st = check_common(g, a, out);
     if (st) return st;
     return eval_sources_device(g, a, nullptr, 0, opts, out);
@@ -3506,6 +3508,7 @@ extern "C" rpq_status rpq_eval_allpairs(const rpq_graph *g, const rpq_nfa *a, co
 
 extern "C" rpq_status rpq_plan(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
                                rpq_plan_info *info) {
+    NvtxRange nvtx_("rpq_plan");
     if (!g || !a || !info) return rpq_fail(RPQ_EINVAL, "NULL argument");
     rpq_eval_opts o{};
     if (opts) o = *opts;
@@ -3524,6 +3527,7 @@ extern "C" rpq_status rpq_plan(const rpq_graph *g, const rpq_nfa *a, const rpq_e
 
 extern "C" rpq_status rpq_eval_sources(const rpq_graph *g, const rpq_nfa *a, const uint32_t *srcs, uint64_t n,
                                        const rpq_eval_opts *opts, rpq_result **out) {
+    NvtxRange nvtx_("rpq_eval_sources");
     rpq_status st = check_common(g, a, out);
     if (st) return st;
     if (n && !srcs) return rpq_fail(RPQ_EINVAL, "NULL sources");
@@ -3549,6 +3553,7 @@ extern "C" rpq_status rpq_eval_sources(const rpq_graph *g, const rpq_nfa *a, con
 extern "C" rpq_status rpq_eval_allpairs_stream(const rpq_graph *g, const rpq_nfa *a, const rpq_eval_opts *opts,
                                                uint64_t device_budget_bytes, uint64_t piece_pairs,
                                                rpq_pairs_sink sink, void *ctx, uint64_t *total) {
+    NvtxRange nvtx_("rpq_eval_allpairs_stream");
     if (total) *total = 0;
     rpq_result *dummy = nullptr;
     rpq_status st = check_common(g, a, &dummy);
@@ -3657,6 +3662,7 @@ extern "C" rpq_status rpq_eval_allpairs_stream(const rpq_graph *g, const rpq_nfa
 // e.g. a (b c)* d runs as a L? d with L = R((b c)+).
 extern "C" rpq_status rpq_cache_closure(rpq_graph *g, const rpq_nfa *inner, const char *name,
                                         const rpq_eval_opts *opts, uint32_t *label_id) {
+    NvtxRange nvtx_("rpq_cache_closure");
     rpq_result *r = nullptr;
     rpq_status st = check_common(g, inner, &r);
     if (st) return st;
@@ -3675,6 +3681,7 @@ extern "C" rpq_status rpq_cache_closure(rpq_graph *g, const rpq_nfa *inner, cons
 // R(loop+) as a fresh derived label L, then evaluate "(prefix) L? (suffix)".
 extern "C" rpq_status rpq_eval_loop_cached(rpq_graph *g, const char *prefix, const char *loop, const char *suffix,
                                            const rpq_eval_opts *opts, rpq_result **out) {
+    NvtxRange nvtx_("rpq_eval_loop_cached");
     if (out) *out = nullptr;
     if (!g || !loop || !out) return rpq_fail(RPQ_EINVAL, "rpq_eval_loop_cached: NULL argument");
     static std::atomic<uint32_t> next_id{0};
@@ -3708,6 +3715,7 @@ extern "C" rpq_status rpq_eval_loop_cached(rpq_graph *g, const char *prefix, con
 
 extern "C" rpq_status rpq_eval_targets(const rpq_graph *g, const rpq_nfa *a, const uint32_t *targets,
                                        uint64_t n, const rpq_eval_opts *opts, rpq_result **out) {
+    NvtxRange nvtx_("rpq_eval_targets");
     rpq_status st = check_common(g, a, out);
     if (st) return st;
     if (g->in_csr.size() != g->csr.size())

@@ -133,6 +133,7 @@ extern "C" void rpq_graph_free(rpq_graph *g) {
 }
 
 extern "C" rpq_status rpq_graph_load(const rpq_graph_desc *d, rpq_graph **out) {
+    NvtxRange nvtx_("rpq_graph_load");
     if (out) *out = nullptr;
     if (!d || !out) return rpq_fail(RPQ_EINVAL, "rpq_graph_load: NULL argument");
     if (d->num_vertices == 0) return rpq_fail(RPQ_EINVAL, "rpq_graph_load: num_vertices == 0");

@@ -8,7 +8,17 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: no-ops unless a profiler tool is attached
+
 #include "rpq.h"
+
+// NVTX range over a C-ABI call (nsys / ncu --nvtx timelines)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ---- error reporting (thread-local message, rpq_last_error) --------------
 rpq_status rpq_fail(rpq_status st, const char *fmt, ...);
