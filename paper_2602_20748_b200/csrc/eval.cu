@@ -1780,40 +1780,59 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
     return x;
 }
 
-// Per-(source, tile) counts by warp bit transposes: a warp takes a tile of
-// TILE_V vertices and a group of 4 words (32 B = one sector per row); lane l
-// holds vertex v0 + l; after the transpose lane b holds the block's members
-// of source w*64+b.  cnt[(i) * nseg + seg] (u32), i = batch-local source index.
-__global__ void k_tile_counts(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo, uint64_t vn,
-                              uint32_t nw, uint32_t nb, uint32_t nseg, uint32_t *cnt) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+// Per-(source, tile) counts by warp bit transposes.  Same task shape and
+// coalesced sector loads as k_write_pairs (below): a CTA of 4 warps takes a
+// group of 4 words (256 sources) and a part of tpp tiles of TILE_V vertices;
+// the 512 x 4 visited words of a tile (OR over the final states) are staged
+// in shared memory and warp w counts, per 32-vertex block of its word, the
+// members of each source (lane b after the transpose: sources 64 w + b and
+// + 32).  cnt[i * nseg + seg] (u32), i = batch-local source index.
+constexpr int TC_XLD = TILE_V + 8;           // words k, k+1 in disjoint bank halves
+__global__ void __launch_bounds__(128) k_tile_counts(const DevAuto A, const Layout S, const uint64_t *Vis, uint32_t vlo,
+                                                     uint64_t vn, uint32_t nw, uint32_t nb, uint32_t nseg, uint32_t tpp,
+                                                     uint32_t *cnt) {
+    __shared__ __align__(16) uint64_t xs[4][TC_XLD];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const uint32_t k = threadIdx.x & 3u, r = threadIdx.x >> 2;
     const uint64_t nwg = (nw + 3) / 4;
-    const uint64_t nwarps = (uint64_t)gridDim.x * blockDim.x >> 5;
-    for (uint64_t task = wid; task < (uint64_t)nseg * nwg; task += nwarps) {
-        const uint32_t seg = (uint32_t)(task / nwg);
-        const uint32_t w0 = (uint32_t)(task % nwg) * 4;
-        uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        const uint64_t vbeg = (uint64_t)seg * TILE_V, vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
-        for (uint64_t v0 = vbeg; v0 < vend; v0 += 32) {
-            const uint64_t vv = v0 + lane;
-            uint64_t x[4];
+    const uint64_t nparts = (nseg + tpp - 1) / tpp;
+    for (uint64_t ct = blockIdx.x; ct < nwg * nparts; ct += gridDim.x) {
+        const uint32_t g = (uint32_t)(ct % nwg);
+        const uint32_t s0 = (uint32_t)(ct / nwg) * tpp, s1 = min(nseg, s0 + tpp);
+        const uint32_t w = g * 4 + (uint32_t)wl, wk = g * 4 + k;
+        for (uint32_t seg = s0; seg < s1; ++seg) {
+            const uint64_t vbeg = (uint64_t)seg * TILE_V, vend = (vn < vbeg + TILE_V ? vn : vbeg + TILE_V);
+            uint64_t xv[TILE_V / 32];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                x[k] = (vv < vend && w0 + k < nw) ? ans_word(A, S, Vis, vlo + (uint32_t)vv, w0 + k, nw) : 0ull;
+            for (int i = 0; i < TILE_V / 32; ++i) xv[i] = 0ull;
+            uint64_t fm = wk < nw ? A.final_mask : 0ull;
+            while (fm) {
+                const int q = __ffsll((long long)fm) - 1;
+                fm &= fm - 1;
+                const uint32_t qlo = S.lo[q], qlen = S.len[q];
+                const uint64_t qb = S.row_base[q];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (!__ballot_sync(0xffffffffu, x[k] != 0)) continue;
-                // lane b: the block's members of sources 64 (w0 + k) + b and + 32 + b
-                c[2 * k] += __popc(warp_transpose32((uint32_t)x[k], lane));
-                c[2 * k + 1] += __popc(warp_transpose32((uint32_t)(x[k] >> 32), lane));
+                for (int i = 0; i < TILE_V / 32; ++i) {
+                    const uint64_t vv = vbeg + r + 32u * (uint32_t)i;
+                    const uint32_t d = vlo + (uint32_t)vv - qlo;
+                    if (vv < vend && d < qlen) xv[i] |= ld_cg(Vis + (qb + d) * nw + wk);
+                }
             }
-        }
+            __syncthreads();                     // the previous tile's rows are consumed
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t i0 = (w0 + k) * 64 + lane, i1 = i0 + 32;
-            if (i0 < nb) cnt[(uint64_t)i0 * nseg + seg] = c[2 * k];
-            if (i1 < nb) cnt[(uint64_t)i1 * nseg + seg] = c[2 * k + 1];
+            for (int i = 0; i < TILE_V / 32; ++i) xs[k][r + 32u * (uint32_t)i] = xv[i];
+            __syncthreads();
+            uint32_t c_lo = 0, c_hi = 0;
+#pragma unroll
+            for (int blk = 0; blk < TILE_V / 32; ++blk) {
+                const uint64_t x = xs[wl][blk * 32 + lane];
+                if (!__ballot_sync(0xffffffffu, x != 0)) continue;
+                c_lo += __popc(warp_transpose32((uint32_t)x, lane));
+                c_hi += __popc(warp_transpose32((uint32_t)(x >> 32), lane));
+            }
+            const uint32_t i0 = w * 64 + (uint32_t)lane, i1 = i0 + 32;
+            if (w < nw && i0 < nb) cnt[(uint64_t)i0 * nseg + seg] = c_lo;
+            if (w < nw && i1 < nb) cnt[(uint64_t)i1 * nseg + seg] = c_hi;
         }
     }
 }
@@ -3303,9 +3322,14 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
         unsigned long long *tot = (unsigned long long *)ws.get((uint64_t)nb * 8);
         if (!cnt || !tot) return fail(rpq_fail(RPQ_ENOMEM, "out of device memory (extraction)"));
         RPQ_CUDA_TRY(cudaMemsetAsync(cnt, 0, (uint64_t)nb * nseg * 4, s));
-        const uint64_t tasks = (uint64_t)nseg * ((nw + 3) / 4);
+        // tile tasks: parts of tpp tiles x groups of 4 words (k_tile_counts, k_write_pairs)
+        const uint64_t nwg = (nw + 3) / 4;
+        const uint64_t nparts = std::min<uint64_t>(nseg, ((uint64_t)148 * 6 * 4 + nwg - 1) / nwg);
+        const uint32_t tpp = (uint32_t)((nseg + nparts - 1) / nparts);
+        const uint64_t ntask = nwg * ((nseg + tpp - 1) / tpp);
         if (vn) {
-            k_tile_counts<<<grid_for(tasks * 32), 256, 0, s>>>(A, S, Vis, vlo, vn, (uint32_t)nw, nb, nseg, cnt);
+            k_tile_counts<<<(unsigned)std::min<uint64_t>(ntask, 148 * 12), 128, 0, s>>>(A, S, Vis, vlo, vn,
+                                                                                     (uint32_t)nw, nb, nseg, tpp, cnt);
             ST.kernel_launches++;
         }
         k_row_scan<<<grid_for((uint64_t)nb * 32), 256, 0, s>>>(cnt, nb, nseg, tot);
@@ -3338,12 +3362,6 @@ static rpq_status eval_sources_impl(const rpq_graph *g, const rpq_nfa *a, const 
             blocks.push_back(bl);
             HM("pairs: cudaMalloc of the block");
             if (vn) {
-                // parts of tpp tiles: ~24 CTA tasks per SM slot for balance
-                const uint64_t nwg = (nw + 3) / 4;
-                const uint64_t want = (uint64_t)148 * 6 * 4;
-                const uint64_t nparts = std::min<uint64_t>(nseg, (want + nwg - 1) / nwg);
-                const uint32_t tpp = (uint32_t)((nseg + nparts - 1) / nparts);
-                const uint64_t ntask = nwg * ((nseg + tpp - 1) / tpp);
                 k_write_pairs<<<(unsigned)std::min<uint64_t>(ntask, 148 * 6), WP_WARPS * 32, 0, s>>>(
                     A, S, Vis, vlo, vn, (uint32_t)nw, nb, nseg, tpp, cnt, cand, pidx, b0, start, jlo, bl.src, bl.dst);
                 ST.kernel_launches++;
