@@ -124,3 +124,37 @@ def test_rmat24_1024_sources_pairs_counts_pe(rmat):
         # (ascending) order: already (src, dst)-sorted, no host sort needed
         want = np.stack([o["src"], o["dst"]], 1).astype(np.uint32)
         assert np.array_equal(r.rows(), want)
+
+
+@pytest.mark.parametrize("rx", ["(a|b)*c*", "a b* c"])
+def test_pairs_multi_tile_parts(rx):
+    """All-pairs PAIRS where the extraction tasks span several 512-vertex
+    tiles (40 K sources x 40 K vertices: 157 word groups x parts of 4 tiles),
+    so per-source runs continue across tiles through the sector-aligned carry;
+    (a|b)*c* has two final states (their rows are OR-ed).  Every source's
+    count against O1, the pair lists of 512 seeded sources element by element,
+    and the (src, dst) order across run boundaries."""
+    g = synth.uniform_graph(40_000, 300_000, 3, seed=7)
+    G = R.rpq_graph_load(g)
+    og = oracle.OracleGraph(g)
+    a = R.rpq_compile(G, rx)
+    r = R.rpq_eval_allpairs(G, a, mode=R.RPQ_PAIRS)
+    s, c = r.source_counts()
+    cnt = np.zeros(g.num_vertices, np.uint64)
+    cnt[s] = c
+    o_all = oracle.eval_sources(og, rx, None, pairs=False, threads=THREADS)
+    assert np.array_equal(cnt, o_all["counts"]), rx
+    start = np.zeros(g.num_vertices + 1, np.uint64)
+    start[1:] = np.cumsum(cnt)
+    assert int(start[-1]) == r.count
+    sample = synth.sample_sources(g.num_vertices, 512, seed=77)
+    o = oracle.eval_sources(og, rx, sample, threads=THREADS)
+    want = sorted_pairs(o["src"], o["dst"])
+    got = np.concatenate([device_rows(r, int(start[v]), int(cnt[v])) for v in sample])
+    assert np.array_equal(got, want), rx
+    # source-major order across run boundaries: windows around sampled starts
+    for v in sample[:64]:
+        lo = max(0, int(start[v]) - 8)
+        w = device_rows(r, lo, min(16, r.count - lo))
+        key = w[:, 0].astype(np.uint64) << np.uint64(32) | w[:, 1].astype(np.uint64)
+        assert bool(np.all(key[1:] > key[:-1])), (rx, v)
