@@ -16,8 +16,8 @@ for r in csv.DictReader(lines):
     if unit == "Gbyte": x *= 1e9
     elif unit == "Mbyte": x *= 1e6
     elif unit == "Kbyte": x *= 1e3
-    elif unit == "msecond": x *= 1e3
-    elif unit == "nsecond": x *= 1e-3
+    elif unit in ("msecond", "ms"): x *= 1e3
+    elif unit in ("nsecond", "ns"): x *= 1e-3
     rows.setdefault(k, {})[r["Metric Name"]] = x
 pat = re.compile(sys.argv[2]) if len(sys.argv) > 2 else None
 tot = {}
